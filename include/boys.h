@@ -1,0 +1,110 @@
+/*
+ * libboys -- B200-native batched Boys-function evaluator (arXiv 2504.07637).
+ *
+ * C ABI (extern "C", plain pointers and sizes, no torch types).  Every entry
+ * point replaces a piece of the reference's SPEC'd kernel interface; the
+ * reference ships it only as a specification, so each comment cites the SPEC
+ * line that defines the behaviour and the refmath line that fixes the output
+ * semantics (index m <-> F_m, recursion F_m = (2x F_{m+1} + e^-x)/(2m+1)).
+ *
+ *   reference interface                                  replaced by
+ *   ---------------------------------------------------  -------------------------
+ *   kernel.eval_batch(EvalRequest{n, xs, layout}, T)      boys_eval_dense
+ *       SPEC.md:316-324; semantics refmath.py:330-341
+ *   kernel.eval_fn(n, x, T) -> (fn, expx)                 boys_eval_dense(n_max=n,
+ *       SPEC.md:298-306                                     expx_dev != NULL)
+ *   kernel.eval_with_split(n, n_bar, x, T)                boys_eval_split
+ *       SPEC.md:325-333
+ *   ragged batches (per-element order)   boys_eval_ragged
+ *   domain error "listing offending indices"              boys_domain_result
+ *       SPEC.md:302, 320, 347; refmath.py:111-115
+ *   order check (refmath.py:104-108, MAX_ORDER :41)       BOYS_E_ORDER / boys_max_order
+ *   eval_batch with host arrays (the CPU caller's view)   boys_eval_dense_host
+ *
+ * Conventions
+ *   - Device pointers are caller-owned, 16-byte aligned for x/out, and the work
+ *     is stream-ordered on `stream` (a cudaStream_t passed as void*; NULL =
+ *     legacy default stream).  No allocation and no host sync on the device
+ *     entry points; tables are compiled into the module (__constant__).
+ *   - Layouts: BOYS_SOA = order-major [n_max+1][N]; BOYS_AOS = point-major
+ *     [N][n_max+1] ("order-major, point-major").
+ *   - Domain: x must be finite and >= 0 (-0.0 is accepted as 0).  Offending
+ *     elements produce NaN outputs; if `dom_dev` is non-NULL the smallest
+ *     offending index is atomically min-reduced into it.  The caller
+ *     initialises *dom_dev to -1 (all bits set) = "no error".
+ *   - Results are bit-identical to the CPU restatement in oracle/ (same
+ *     operation sequence, explicit FMA, IEEE div/sqrt, shared exp algorithm).
+ */
+#ifndef BOYS_H_
+#define BOYS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  BOYS_OK = 0,
+  BOYS_E_DOMAIN = 1,  /* some x < 0, NaN or inf (only from *_host / domain_result) */
+  BOYS_E_ORDER = 2,   /* n_max < 0 or above boys_max_order(dtype) */
+  BOYS_E_LAYOUT = 3,
+  BOYS_E_DTYPE = 4,
+  BOYS_E_ALIGN = 5,   /* x/out not 16-byte aligned, or bad sizes */
+  BOYS_E_CUDA = 6,    /* CUDA runtime error (see boys_last_cuda_error) */
+  BOYS_E_ARG = 7      /* NULL pointer / negative N / bad split */
+} boys_status;
+
+typedef enum { BOYS_F64 = 0, BOYS_F32 = 1 } boys_dtype;
+typedef enum { BOYS_SOA = 0, BOYS_AOS = 1 } boys_layout;
+
+/* Highest tabulated order for the dtype (16 for f64, 8 for f32). */
+int boys_max_order(boys_dtype dtype);
+
+/* Library / table version string ("libboys <ver> tables <sha-prefix>"). */
+const char* boys_version(void);
+
+/* F_0..F_{n_max}(x_i) for i < N into out_dev (layout as above).
+ * expx_dev (nullable): e^{-x_i} as used by the recursion (0 for x > 708 / 87). */
+boys_status boys_eval_dense(boys_dtype dtype, int n_max, const void* x_dev, int64_t N,
+                            void* out_dev, boys_layout layout, void* expx_dev,
+                            int64_t* dom_dev, void* stream);
+
+/* Ragged batch: element i has its own order nmax_dev[i] (0..boys_max_order)
+ * and writes F_0..F_{n_i} to out_dev[offsets_dev[i] + m]; offsets_dev has N+1
+ * entries (exclusive prefix sum of n_i + 1).  Values are bit-identical to
+ * boys_eval_dense at order n_i for the same x. */
+boys_status boys_eval_ragged(boys_dtype dtype, const void* x_dev, const uint8_t* nmax_dev,
+                             const int64_t* offsets_dev, int64_t N, void* out_dev,
+                             int64_t* dom_dev, void* stream);
+
+/* offsets_dev[0] = 0, offsets_dev[i+1] = offsets_dev[i] + nmax_dev[i] + 1. */
+boys_status boys_ragged_offsets(const uint8_t* nmax_dev, int64_t N, int64_t* offsets_dev,
+                                void* stream);
+
+/* eval_with_split: F_n seeds the recursion n -> n_bar+1 and
+ * an independent F_{n_bar} seeds n_bar -> 0.  0 <= n_bar < n. */
+boys_status boys_eval_split(boys_dtype dtype, int n, int n_bar, const void* x_dev, int64_t N,
+                            void* out_dev, boys_layout layout, int64_t* dom_dev, void* stream);
+
+/* Synchronises `stream`, copies *dom_dev to *first_bad (-1 = all valid). */
+boys_status boys_domain_result(const int64_t* dom_dev, int64_t* first_bad, void* stream);
+
+/* Host-buffer entry (end-to-end path): x_host[N] -> out_host in `layout`,
+ * pipelined host->device copy / kernel / device->host copy over chunks on the
+ * current device.  Blocks until done.  Host buffers should be pinned for full
+ * link speed.  Returns BOYS_E_DOMAIN (and *first_bad) if some x is invalid. */
+boys_status boys_eval_dense_host(boys_dtype dtype, int n_max, const void* x_host, int64_t N,
+                                 void* out_host, boys_layout layout, int64_t* first_bad);
+
+/* Number of kernel launches issued by this library in this process. */
+int64_t boys_launch_count(void);
+
+const char* boys_status_str(boys_status s);
+const char* boys_last_cuda_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BOYS_H_ */

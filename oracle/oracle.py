@@ -1,0 +1,133 @@
+"""ctypes wrapper of the CPU oracle (liboracle.so) -- TEST INFRASTRUCTURE.
+
+Only tests/, __graft_entry__.smoke() and bench.py's CPU-baseline / reference
+arm may import this module, and only as the checker.  The product path
+(paper_2504_07637_b200) never imports it.
+
+The oracle restates the SPEC'd kernel in C; see
+boys_oracle.c for the line-by-line citations and the pinning strategy.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import subprocess
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+ROOT = HERE.parent
+LIB = HERE / "liboracle.so"
+DATA = ROOT / "paper_2504_07637_b200" / "data"
+
+_lib = None
+_tables = {}
+
+
+def build(force: bool = False) -> Path:
+    if force or not LIB.exists() or LIB.stat().st_mtime < max(
+            (HERE / f).stat().st_mtime for f in ("boys_oracle.c", "boys_oracle_impl.h")):
+        subprocess.run(["make", "-s", "-C", str(HERE)], check=True)
+    return LIB
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = C.CDLL(str(LIB))
+        L.boys_oracle_load.restype = C.c_void_p
+        L.boys_oracle_load.argtypes = [C.c_char_p]
+        L.boys_oracle_max_order.argtypes = [C.c_void_p]
+        L.boys_oracle_dense.restype = C.c_int64
+        L.boys_oracle_dense.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_void_p,
+                                        C.c_int, C.c_void_p]
+        L.boys_oracle_ragged.restype = C.c_int64
+        L.boys_oracle_ragged.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                         C.c_int64, C.c_void_p]
+        L.boys_oracle_split.restype = C.c_int64
+        L.boys_oracle_split.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int64,
+                                        C.c_void_p, C.c_int]
+        L.boys_oracle_qtilde.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_void_p]
+        L.boys_oracle_expneg.argtypes = [C.c_int, C.c_void_p, C.c_int64, C.c_void_p]
+        L.boys_oracle_threads.restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def table(dtype):
+    dtype = np.dtype(dtype)
+    if dtype not in _tables:
+        prof = "single24" if dtype == np.float32 else "double53"
+        t = lib().boys_oracle_load(str(DATA / f"boys_{prof}.dat").encode())
+        if not t:
+            raise RuntimeError(f"oracle could not parse the {prof} dataset")
+        _tables[dtype] = t
+    return _tables[dtype]
+
+
+def max_order(dtype) -> int:
+    return lib().boys_oracle_max_order(table(dtype))
+
+
+def _ptr(a):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def dense(n: int, x, layout: str = "soa", expx: bool = False):
+    """F_0..F_n for every x (dtype float64 or float32).  Returns
+    (values, first_bad[, expx]); values [n+1][N] (soa) or [N][n+1] (aos)."""
+    x = np.ascontiguousarray(x)
+    assert x.dtype in (np.float64, np.float32)
+    N = x.size
+    shape = (n + 1, N) if layout == "soa" else (N, n + 1)
+    out = np.empty(shape, dtype=x.dtype)
+    ex = np.empty(N, dtype=x.dtype) if expx else None
+    bad = lib().boys_oracle_dense(table(x.dtype), n, _ptr(x), N, _ptr(out),
+                                  0 if layout == "soa" else 1, _ptr(ex) if expx else None)
+    return (out, bad, ex) if expx else (out, bad)
+
+
+def offsets(nmax):
+    nmax = np.asarray(nmax, dtype=np.uint8)
+    off = np.zeros(nmax.size + 1, dtype=np.int64)
+    np.cumsum(nmax.astype(np.int64) + 1, out=off[1:])
+    return off
+
+
+def ragged(x, nmax):
+    x = np.ascontiguousarray(x)
+    nmax = np.ascontiguousarray(nmax, dtype=np.uint8)
+    off = offsets(nmax)
+    out = np.empty(int(off[-1]), dtype=x.dtype)
+    bad = lib().boys_oracle_ragged(table(x.dtype), _ptr(x), _ptr(nmax), _ptr(off), x.size,
+                                   _ptr(out))
+    return out, off, bad
+
+
+def split(n: int, nbar: int, x, layout: str = "soa"):
+    x = np.ascontiguousarray(x)
+    N = x.size
+    out = np.empty((n + 1, N) if layout == "soa" else (N, n + 1), dtype=x.dtype)
+    bad = lib().boys_oracle_split(table(x.dtype), n, nbar, _ptr(x), N, _ptr(out),
+                                  0 if layout == "soa" else 1)
+    return out, bad
+
+
+def qtilde(n: int, x):
+    x = np.ascontiguousarray(x)
+    out = np.empty_like(x)
+    lib().boys_oracle_qtilde(table(x.dtype), n, _ptr(x), x.size, _ptr(out))
+    return out
+
+
+def expneg(x):
+    x = np.ascontiguousarray(x)
+    out = np.empty_like(x)
+    lib().boys_oracle_expneg(int(x.dtype == np.float32), _ptr(x), x.size, _ptr(out))
+    return out
+
+
+def threads() -> int:
+    return lib().boys_oracle_threads()

@@ -1,0 +1,222 @@
+"""GPU parity: libboys (sm_100a) vs the CPU oracle on identical seeded inputs.
+
+Contract (BASELINE.json north_star): <= 8 ulp relative in fp64 and a per-n
+bound in fp32.  Design target, asserted separately: 0 ulp (bit-identical),
+since the kernel and the oracle execute the same IEEE operation sequence.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2504_07637_b200 import boys, boys_ragged, eval_batch, eval_fn, eval_with_split
+from paper_2504_07637_b200 import EvalRequest, max_order, workloads as W
+from paper_2504_07637_b200 import _lib
+
+pytestmark = pytest.mark.gpu
+
+ULP_TOL = {np.float64: 8, np.float32: 2}   # contract; the design target is 0
+
+
+def ulp_diff(a: np.ndarray, b: np.ndarray) -> np.ndarray:
+    """|a - b| in units of the last place, via the ordered integer view."""
+    assert a.dtype == b.dtype
+    it = np.int64 if a.dtype == np.float64 else np.int32
+    ia = a.view(it).astype(np.int64)
+    ib = b.view(it).astype(np.int64)
+    sign = np.int64(1) << (63 if it == np.int64 else 31)
+    ia = np.where(ia < 0, -(ia & ~sign) if it == np.int64 else -(ia & 0x7FFFFFFF), ia)
+    ib = np.where(ib < 0, -(ib & ~sign) if it == np.int64 else -(ib & 0x7FFFFFFF), ib)
+    d = np.abs(ia - ib)
+    both_nan = np.isnan(a) & np.isnan(b)
+    return np.where(both_nan, 0, d)
+
+
+def assert_parity(got: np.ndarray, ref: np.ndarray, what: str):
+    assert got.shape == ref.shape, what
+    assert np.array_equal(np.isnan(got), np.isnan(ref)), f"{what}: NaN pattern differs"
+    d = ulp_diff(got, ref)
+    tol = ULP_TOL[got.dtype.type]
+    assert d.max(initial=0) <= tol, f"{what}: max {d.max()} ulp > {tol}"
+    nbad = int((d != 0).sum())
+    assert nbad == 0, f"{what}: {nbad} values not bit-identical (max {d.max()} ulp)"
+
+
+def edge_x(dtype, n):
+    """Edge cases: zeros, denormals, cut-off neighbourhoods, exp cut, x_up, max."""
+    from paper_2504_07637_b200 import coeffs as C
+    ds = C.load_default("single24" if dtype == np.float32 else "double53")
+    r = ds.records[n]
+    fi = np.finfo(dtype)
+    xexp = 86.0 if dtype == np.float32 else 708.0
+    vals = [0.0, -0.0, fi.smallest_subnormal, fi.tiny, 1e-30, 1e-12, 1e-6, 0.5, 1.0, 2.0,
+            r.z, r.x_up, xexp, 20.0, 30.0, 40.0, 100.0, 1e3, 1e4, 1e6, 1e9, 1e15, 1e18,
+            1e20, 1e30, fi.max / 2, fi.max]
+    out = []
+    for v in vals:
+        v = dtype(v)
+        out += [v, np.nextafter(v, dtype(np.inf)), np.nextafter(v, dtype(0))]
+    for k in range(1, 64):
+        out.append(dtype(r.z * (1 + (k - 32) * 1e-4)))
+    return np.array([v for v in out if v >= 0 and np.isfinite(v)], dtype=dtype)
+
+
+def dense_inputs(dtype, n, N=1 << 16, seed=7):
+    z = {}
+    rng = np.random.default_rng(seed + n)
+    a = rng.uniform(0, 80, N // 4)
+    b = np.exp(rng.uniform(np.log(1e-12), np.log(1e7), N // 4))
+    c = rng.uniform(0, 1, N // 4)
+    d = np.exp(rng.uniform(np.log(1e-3), np.log(800), N - 3 * (N // 4)))
+    x = np.concatenate([a, b, c, d]).astype(dtype)
+    rng.shuffle(x)
+    return np.concatenate([edge_x(dtype, n), x])
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("layout", ["soa", "aos"])
+def test_dense_all_orders_bit_exact(oracle, dtype, layout):
+    for n in range(max_order(dtype) + 1):
+        x = dense_inputs(dtype, n, N=4099)
+        got = boys(n, torch.from_numpy(x).cuda(), layout=layout).cpu().numpy()
+        ref, bad = oracle.dense(n, x, layout)
+        assert bad == -1
+        assert_parity(got, ref, f"n={n} {layout} {dtype.__name__}")
+
+
+@pytest.mark.parametrize("cfg", ["cfg1", "cfg2", "cfg3", "cfg5"])
+def test_config_inputs_bit_exact(oracle, cfg):
+    c = W.CONFIGS[cfg]
+    x = W.config_x(cfg, n=1 << 20, device="cuda")
+    got = boys(c.n_max, x, layout=c.layout).cpu().numpy()
+    ref, bad = oracle.dense(c.n_max, x.cpu().numpy(), c.layout)
+    assert bad == -1
+    assert_parity(got, ref, cfg)
+
+
+@pytest.mark.parametrize("N", [0, 1, 2, 255, 256, 257, 1000, 65537])
+def test_sizes_and_tails(oracle, N):
+    for n, layout in ((16, "aos"), (12, "aos"), (8, "soa"), (3, "aos")):
+        x = np.abs(np.random.default_rng(N).standard_normal(N)) * 30
+        got = boys(n, torch.from_numpy(x).cuda(), layout=layout).cpu().numpy()
+        ref, _ = oracle.dense(n, x, layout)
+        assert_parity(got, ref, f"N={N} n={n} {layout}")
+
+
+def test_unaligned_out_falls_back(oracle):
+    # AoS output pointer offset by one element (8 B): bulk stores must be off
+    n, N = 16, 5000
+    x = np.random.default_rng(0).uniform(0, 90, N)
+    base = torch.empty(N * (n + 1) + 1, dtype=torch.float64, device="cuda")
+    out = base[1:].view(N, n + 1)
+    boys(n, torch.from_numpy(x).cuda(), layout="aos", out=out)
+    ref, _ = oracle.dense(n, x, "aos")
+    assert_parity(out.cpu().numpy(), ref, "unaligned aos")
+
+
+def test_expx_and_eval_fn(oracle):
+    x = dense_inputs(np.float64, 5, N=2048)
+    res = eval_batch(EvalRequest(n=5, xs=torch.from_numpy(x).cuda()))
+    ref, _, ex = oracle.dense(5, x, "soa", expx=True)
+    assert_parity(res.values.cpu().numpy(), ref, "eval_batch")
+    assert_parity(res.expx.cpu().numpy(), ex, "expx")
+    fn, t = eval_fn(5, 3.25)
+    r1, _, e1 = oracle.dense(5, np.array([3.25]), "soa", expx=True)
+    assert fn == r1[5, 0] and t == e1[0]
+
+
+def test_host_path_matches_device(oracle):
+    for dtype, n, layout in ((np.float64, 16, "aos"), (np.float64, 8, "soa"),
+                             (np.float32, 8, "aos"), (np.float32, 5, "soa")):
+        x = dense_inputs(dtype, n, N=(1 << 22) + 77)     # several pipeline chunks
+        got = boys(n, x, layout=layout)
+        assert isinstance(got, np.ndarray)
+        ref, _ = oracle.dense(n, x, layout)
+        assert_parity(got, ref, f"host {dtype.__name__} n={n} {layout}")
+
+
+def test_domain_errors():
+    x = torch.tensor([1.0, -1.0, 2.0, float("nan"), float("inf"), 0.0], device="cuda",
+                     dtype=torch.float64)
+    with pytest.raises(ValueError, match=r"offending indices \[1, 3, 4\]"):
+        boys(4, x)
+    with pytest.raises(ValueError, match=r"offending indices \[1, 3, 4\]"):
+        boys(4, x.cpu().numpy())
+    out = boys(4, x, check=False).cpu().numpy()     # lanes are NaN, others valid
+    assert np.isnan(out[:, [1, 3, 4]]).all() and np.isfinite(out[:, [0, 2, 5]]).all()
+    with pytest.raises(ValueError, match="exceeds the supported maximum"):
+        boys(17, x.abs())
+    with pytest.raises(ValueError, match="exceeds the supported maximum"):
+        boys(9, x.abs().float())
+    with pytest.raises(ValueError, match="non-negative integer"):
+        boys(-1, x.abs())
+    with pytest.raises(ValueError, match="layout"):
+        boys(2, x.abs(), layout="diagonal")
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_ragged_bit_exact_and_equals_dense(oracle, dtype):
+    mx = max_order(dtype)
+    rng = np.random.default_rng(3)
+    x = dense_inputs(dtype, mx, N=20000)
+    nm = rng.integers(0, mx + 1, size=x.size).astype(np.uint8)
+    got, off = boys_ragged(torch.from_numpy(x).cuda(), torch.from_numpy(nm).cuda())
+    ref, roff, bad = oracle.ragged(x, nm)
+    assert bad == -1
+    assert np.array_equal(off.cpu().numpy(), roff)
+    got = got.cpu().numpy()
+    assert_parity(got, ref, f"ragged {dtype.__name__}")
+    for n in range(mx + 1):   # ragged == dense at each element's order
+        sel = np.nonzero(nm == n)[0][:500]
+        d = boys(n, torch.from_numpy(x[sel]).cuda(), layout="aos").cpu().numpy()
+        for j, i in enumerate(sel):
+            assert np.array_equal(got[roff[i]:roff[i + 1]], d[j], equal_nan=True)
+
+
+def test_ragged_cfg4_inputs(oracle):
+    x, nm = W.cfg4_batch(1 << 20, device="cuda")
+    got, off = boys_ragged(x, nm)
+    ref, roff, bad = oracle.ragged(x.cpu().numpy(), nm.cpu().numpy())
+    assert bad == -1
+    assert_parity(got.cpu().numpy(), ref, "cfg4 f64")
+    xf, nf = W.cfg4f32_batch(1 << 20, device="cuda")
+    got, off = boys_ragged(xf, nf)
+    ref, roff, bad = oracle.ragged(xf.cpu().numpy(), nf.cpu().numpy())
+    assert_parity(got.cpu().numpy(), ref, "cfg4 f32")
+
+
+def test_ragged_domain_and_order_errors():
+    x = torch.tensor([1.0, 2.0, -3.0], device="cuda", dtype=torch.float64)
+    nm = torch.tensor([1, 2, 3], device="cuda", dtype=torch.uint8)
+    with pytest.raises(ValueError, match=r"offending indices \[2\]"):
+        boys_ragged(x, nm)
+    nm2 = torch.tensor([1, 40, 3], device="cuda", dtype=torch.uint8)
+    with pytest.raises(ValueError, match="exceeds the supported maximum"):
+        boys_ragged(x.abs(), nm2)
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_split_bit_exact(oracle, dtype):
+    mx = max_order(dtype)
+    x = dense_inputs(dtype, mx, N=3000)
+    for n, nbar in ((mx, mx - 1), (mx, 0), (mx, mx // 2), (3, 1), (1, 0)):
+        for layout in ("soa", "aos"):
+            got = eval_with_split(n, nbar, torch.from_numpy(x).cuda(), layout=layout)
+            ref, bad = oracle.split(n, nbar, x, layout)
+            assert_parity(got.cpu().numpy(), ref, f"split {n}/{nbar} {layout}")
+    # n_bar = n-1: low segment identical to a direct eval at n_bar
+    lo = boys(mx - 1, torch.from_numpy(x).cuda()).cpu().numpy()
+    sp = eval_with_split(mx, mx - 1, torch.from_numpy(x).cuda()).cpu().numpy()
+    assert np.array_equal(sp[:mx], lo, equal_nan=True)
+
+
+def test_stream_ordering_and_launch_count():
+    s = torch.cuda.Stream()
+    x = torch.rand(1 << 20, dtype=torch.float64, device="cuda") * 50
+    before = _lib.launch_count()
+    with torch.cuda.stream(s):
+        a = boys(12, x, layout="aos", check=False)
+    s.synchronize()
+    b = boys(12, x, layout="aos")
+    assert torch.equal(a, b)
+    assert _lib.launch_count() >= before + 2
