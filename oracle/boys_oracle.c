@@ -225,7 +225,7 @@ int64_t boys_oracle_dense(const void* t, int n, const void* x, int64_t N, void* 
                           void* expx) {
   const oracle_table* ot = t;
   const int W = n + 1;
-  int64_t first_bad = -1;
+  int64_t first_bad = INT64_MAX;
 #pragma omp parallel for schedule(static) reduction(min : first_bad)
   for (int64_t i = 0; i < N; ++i) {
     int ok;
@@ -242,16 +242,16 @@ int64_t boys_oracle_dense(const void* t, int n, const void* x, int64_t N, void* 
         ((double*)out)[layout ? i * W + m : (int64_t)m * N + i] = F[m];
       if (expx) ((double*)expx)[i] = tt;
     }
-    if (!ok && (first_bad < 0 || i < first_bad)) first_bad = i;
+    if (!ok && i < first_bad) first_bad = i;
   }
-  return first_bad;
+  return first_bad == INT64_MAX ? -1 : first_bad;
 }
 
 /* Ragged batch: element i of order nmax[i] at out[offsets[i] + m]. */
 int64_t boys_oracle_ragged(const void* t, const void* x, const uint8_t* nmax,
                            const int64_t* offsets, int64_t N, void* out) {
   const oracle_table* ot = t;
-  int64_t first_bad = -1;
+  int64_t first_bad = INT64_MAX;
 #pragma omp parallel for schedule(static) reduction(min : first_bad)
   for (int64_t i = 0; i < N; ++i) {
     int n = nmax[i], ok;
@@ -266,9 +266,9 @@ int64_t boys_oracle_ragged(const void* t, const void* x, const uint8_t* nmax,
     } else {
       ok = point_f64(&ot->t64, n, ((const double*)x)[i], (double*)out + offsets[i], NULL);
     }
-    if (!ok && (first_bad < 0 || i < first_bad)) first_bad = i;
+    if (!ok && i < first_bad) first_bad = i;
   }
-  return first_bad;
+  return first_bad == INT64_MAX ? -1 : first_bad;
 }
 
 /* eval_with_split: F_0..F_nbar from the order-nbar seed,
@@ -277,7 +277,7 @@ int64_t boys_oracle_split(const void* t, int n, int nbar, const void* x, int64_t
                           int layout) {
   const oracle_table* ot = t;
   const int W = n + 1;
-  int64_t first_bad = -1;
+  int64_t first_bad = INT64_MAX;
 #pragma omp parallel for schedule(static) reduction(min : first_bad)
   for (int64_t i = 0; i < N; ++i) {
     int ok;
@@ -294,9 +294,9 @@ int64_t boys_oracle_split(const void* t, int n, int nbar, const void* x, int64_t
       for (int m = 0; m < W; ++m)
         ((double*)out)[layout ? i * W + m : (int64_t)m * N + i] = m <= nbar ? Fl[m] : Fh[m];
     }
-    if (!ok && (first_bad < 0 || i < first_bad)) first_bad = i;
+    if (!ok && i < first_bad) first_bad = i;
   }
-  return first_bad;
+  return first_bad == INT64_MAX ? -1 : first_bad;
 }
 
 /* Q~_n(x) alone (eval_qtilde), for SPEC.md:295-297 checks. */

@@ -1,0 +1,81 @@
+"""The C-ABI library loads and exports every symbol include/boys.h declares;
+the product path has no CPU fallback and never touches oracle/.  (No compute
+calls here: this file runs without a GPU.)"""
+
+import ctypes
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+HEADER = ROOT / "include" / "boys.h"
+
+
+def declared_functions():
+    text = HEADER.read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(boys_[a-z_0-9]+)\s*\(", text)))
+
+
+def test_header_declares_expected_surface():
+    from paper_2504_07637_b200 import _lib
+    assert declared_functions() == sorted(_lib.EXPORTS)
+
+
+def test_library_loads_and_exports_every_symbol():
+    from paper_2504_07637_b200 import _lib
+    L = _lib.load()
+    for name in declared_functions():
+        assert hasattr(L, name), name
+    assert L.boys_max_order(_lib.BOYS_F64) == 16
+    assert L.boys_max_order(_lib.BOYS_F32) == 8
+    assert L.boys_max_order(7) == -1
+    assert b"sm_100a" in L.boys_version()
+    for code in range(8):
+        assert L.boys_status_str(code)
+
+
+def test_argument_errors_without_gpu():
+    """Argument validation happens before any CUDA call."""
+    from paper_2504_07637_b200 import _lib
+    L = _lib.load()
+    x = np.zeros(4)
+    p = x.ctypes.data_as(ctypes.c_void_p)
+    assert L.boys_eval_dense(_lib.BOYS_F64, 17, p, 4, p, 0, None, None, None) == _lib.BOYS_E_ORDER
+    assert L.boys_eval_dense(_lib.BOYS_F32, 9, p, 4, p, 0, None, None, None) == _lib.BOYS_E_ORDER
+    assert L.boys_eval_dense(_lib.BOYS_F64, 2, p, 4, p, 5, None, None, None) == _lib.BOYS_E_LAYOUT
+    assert L.boys_eval_dense(9, 2, p, 4, p, 0, None, None, None) == _lib.BOYS_E_DTYPE
+    assert L.boys_eval_dense(_lib.BOYS_F64, 2, None, 4, p, 0, None, None, None) == _lib.BOYS_E_ARG
+    assert L.boys_eval_dense(_lib.BOYS_F64, 2, p, -1, p, 0, None, None, None) == _lib.BOYS_E_ARG
+    assert L.boys_eval_dense(_lib.BOYS_F64, 2, p, 0, p, 0, None, None, None) == _lib.BOYS_OK
+    bad = ctypes.c_void_p(x.ctypes.data + 4)
+    assert L.boys_eval_dense(_lib.BOYS_F64, 2, bad, 4, p, 0, None, None, None) == _lib.BOYS_E_ALIGN
+    assert L.boys_eval_split(_lib.BOYS_F64, 4, 4, p, 4, p, 0, None, None) == _lib.BOYS_E_ARG
+
+
+def test_no_cpu_fallback():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_2504_07637_b200 import boys
+    with pytest.raises(RuntimeError, match="CUDA"):
+        boys(3, np.array([1.0, 2.0]))
+
+
+def test_product_never_imports_oracle():
+    pkg = ROOT / "paper_2504_07637_b200"
+    for f in list(pkg.rglob("*.py")) + list(pkg.rglob("*.cu")) + list(pkg.rglob("*.cuh")):
+        txt = f.read_text()
+        assert "oracle" not in re.sub(r"#.*|//.*", "", txt).replace("oracle/", ""), f
+    nm = (pkg / "libboys.so").read_bytes()
+    assert b"boys_oracle" not in nm
+
+
+def test_oracle_library_exports():
+    from oracle import oracle as O
+    L = O.lib()
+    for s in ("boys_oracle_load", "boys_oracle_dense", "boys_oracle_ragged", "boys_oracle_split",
+              "boys_oracle_qtilde", "boys_oracle_expneg"):
+        assert hasattr(L, s)
