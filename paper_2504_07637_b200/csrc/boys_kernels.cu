@@ -260,45 +260,194 @@ __device__ __forceinline__ void eval_point_rt(T x_in, bool ok, int n, const Smem
 
 // ---------------------------------------------------------------------------
 // ragged kernel: element i, order n_i, values at out[offsets[i] + m]
+//
+// Per 256-element tile:
+//   stage    x, n, local output offset into shared memory; ballot-compact the
+//            elements that need e^{-x} (x <= XEXP) and those below their
+//            cut-off (x < z_{n_i}) into two lists; counting-sort the tile by
+//            order n_i.
+//   phase A  threads sweep the compacted lists: e^{-x}, then Q~ / s / y with
+//            the run-time-order evaluator (per-lane tables from shared memory)
+//            -- only ~28% / ~5% of ERI-like elements pay for these.
+//   phase B  each thread takes one element of the order-sorted tile; a warp
+//            loops over the (usually one or two) distinct orders it holds and
+//            runs the compile-time-order tail (r = 1/y, F_n, recursion,
+//            upward ladder) for that order, writing into the staged tile.
+//   store    the tile's contiguous output range leaves with coalesced
+//            streaming stores.
+// Every value is bit-identical to boys_eval_dense at the element's order.
+// Tiles holding an order above the table fall back to direct NaN writes.
 // ---------------------------------------------------------------------------
+template <typename T, int NB>
+struct RaggedSmem {
+  SmemTable<T> st;
+  T obuf[kThreads * (NB + 1)];
+  T sx[kThreads], sy[kThreads], stt[kThreads];
+  int soff[kThreads];
+  int hist[NB + 2];
+  short perm[kThreads];
+  short listE[kThreads], listQ[kThreads];
+  unsigned char sn[kThreads], sok[kThreads];
+  int nE, nQ;
+};
+
+// F_n from y (= x past the cut-off) and the recursion/upward ladder, written
+// to dst[0..n].  `mask` = lanes of this warp holding order n.
+template <typename T, int n>
+__device__ __forceinline__ void tail_store(T x, T y, T t, bool ok, unsigned mask, T* dst) {
+  using A = Ar<T>;
+  const BoysRow<T>& R = Tab<T>::row(n);
+  T Fv[n + 1];
+  T r = A::rcp(y);
+  T sr = A::sqrt(r);
+  Fv[n] = n == 0 ? A::mul(R.c, sr) : A::mul(A::mul(R.c, powi<T, (n == 0 ? 1 : n)>(r)), sr);
+  T tx = A::add(x, x);
+#pragma unroll
+  for (int m = n - 1; m >= 0; --m) Fv[m] = A::mul(A::fma(tx, Fv[m + 1], t), rinv<T>(m));
+  bool up = ok && x > R.x_up;
+  if (__any_sync(mask, up)) {
+    T rx = A::rcp(x);
+    T f = up_first(x);
+    Fv[0] = up ? f : Fv[0];
+#pragma unroll
+    for (int m = 0; m < n; ++m) {
+      f = up_next(f, m, rx);
+      Fv[m + 1] = up ? f : Fv[m + 1];
+    }
+  }
+#pragma unroll
+  for (int m = 0; m <= n; ++m) dst[m] = ok ? Fv[m] : A::nan();
+}
+
+template <typename T, int NB, int n = 0>
+__device__ __forceinline__ void tail_dispatch(int nn, T x, T y, T t, bool ok, unsigned mask,
+                                              T* dst) {
+  if constexpr (n <= NB) {
+    if (nn == n) tail_store<T, n>(x, y, t, ok, mask, dst);
+    else tail_dispatch<T, NB, n + 1>(nn, x, y, t, ok, mask, dst);
+  }
+}
+
 template <typename T, int NB>
 __global__ void __launch_bounds__(kThreads)
 ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
               const int64_t* __restrict__ OFF, int64_t N, T* __restrict__ out,
               int64_t* __restrict__ dom) {
+  using A = Ar<T>;
   constexpr int MQ = MaxShape<T>::Q(), ML = MaxShape<T>::L();
-  __shared__ SmemTable<T> st;
-  __shared__ T obuf[kThreads * (NB + 1)];
-  stage_table(st);
-  __syncthreads();
-  const int tid = threadIdx.x;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  RaggedSmem<T, NB>& S = *reinterpret_cast<RaggedSmem<T, NB>*>(smem_raw);
+  stage_table(S.st);
+  const int tid = threadIdx.x, lane = tid & 31;
   const int64_t ntiles = (N + kThreads - 1) / kThreads;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t i0 = tile * kThreads;
     const int64_t i = i0 + tid;
     const bool in = i < N;
     const int64_t last = (i0 + kThreads < N) ? i0 + kThreads : N;
-    const int64_t base = OFF[i0];
-    const int64_t cnt = OFF[last] - base;
+    const int64_t base = __ldg(OFF + i0);
+    const int64_t cnt = __ldg(OFF + last) - base;
     T x = in ? ldg_nc(X + i) : T(0);
-    int n = in ? (int)NM[i] : 0;
-    const int64_t off = in ? OFF[i] - base : 0;
-    bool ok = valid_x(x) && n <= NB;
-    if (in && !ok) flag_domain(dom, i);
-    ok = ok || !in;
-    T Fv[NB + 1];
-    T t;
-    eval_point_rt<T, NB, MQ, ML>(x, ok, n, st, Fv, t);
-    __syncthreads();   // obuf free (previous tile copied out)
-    if (in) {
-      const int nw = n <= NB ? n : NB;
-#pragma unroll
-      for (int m = 0; m <= NB; ++m)
-        if (m <= nw) obuf[off + m] = Fv[m];
+    const int n = in ? (int)NM[i] : 0;
+    const int64_t off = in ? __ldg(OFF + i) - base : 0;
+    const bool xok = valid_x(x);
+    if (in && !(xok && n <= NB)) flag_domain(dom, i);
+    if (tid < NB + 2) S.hist[tid] = 0;
+    if (tid == 0) { S.nE = 0; S.nQ = 0; }
+    __syncthreads();   // previous tile fully stored; table staged (first pass)
+    if (__syncthreads_or(in && n > NB)) {
+      // invalid order somewhere in the tile: direct writes, NaN for the bad ones
+      if (in) {
+        T* dst = out + base + off;
+        if (n > NB || !xok) {
+          for (int m = 0; m <= n; ++m) dst[m] = A::nan();
+        } else {
+          T Fv[NB + 1], t;
+          eval_point_rt<T, NB, MQ, ML>(x, true, n, S.st, Fv, t);
+          for (int m = 0; m <= n; ++m) dst[m] = Fv[m];
+        }
+      } else {
+        T Fv[NB + 1], t;
+        eval_point_rt<T, NB, MQ, ML>(T(0), true, 0, S.st, Fv, t);   // keep warps converged
+      }
+      continue;
+    }
+    const bool ok = in && xok;
+    const T xs = ok ? x : T(0);
+    const bool needE = ok && xs <= A::XEXP;
+    const bool needQ = ok && xs < S.st.row[n].z;
+    // stage + compaction (warp-aggregated atomics)
+    S.sx[tid] = xs;
+    S.sy[tid] = xs;
+    S.stt[tid] = T(0);
+    S.sn[tid] = (unsigned char)n;
+    S.sok[tid] = ok;
+    S.soff[tid] = (int)off;
+    {
+      unsigned bE = __ballot_sync(0xffffffffu, needE), bQ = __ballot_sync(0xffffffffu, needQ);
+      int baseE = 0, baseQ = 0;
+      if (lane == 0) {
+        baseE = atomicAdd(&S.nE, __popc(bE));
+        baseQ = atomicAdd(&S.nQ, __popc(bQ));
+      }
+      baseE = __shfl_sync(0xffffffffu, baseE, 0);
+      baseQ = __shfl_sync(0xffffffffu, baseQ, 0);
+      unsigned lt = (1u << lane) - 1u;
+      if (needE) S.listE[baseE + __popc(bE & lt)] = (short)tid;
+      if (needQ) S.listQ[baseQ + __popc(bQ & lt)] = (short)tid;
+    }
+    int rank_in_bin = in ? atomicAdd(&S.hist[n], 1) : 0;
+    __syncthreads();
+    // phase A1: e^{-x} on the compacted list
+    for (int k = tid; k < S.nE; k += kThreads) {
+      int e = S.listE[k];
+      S.stt[e] = exp_neg_clamped(S.sx[e]);
+    }
+    if (tid == 0) {   // exclusive scan of the order histogram
+      int acc = 0;
+      for (int b = 0; b <= NB; ++b) {
+        int h = S.hist[b];
+        S.hist[b] = acc;
+        acc += h;
+      }
+    }
+    __syncthreads();
+    // phase A2: y = x + Q~^{n+1/2} e^{-x} for elements below their cut-off
+    for (int k = tid; k < S.nQ; k += kThreads) {
+      int e = S.listQ[k];
+      int ne = S.sn[e];
+      const BoysRow<T>& R = S.st.row[ne];
+      T xe = S.sx[e];
+      T u = factored_rt<T, MQ, ML>(xe, R.uq, R.ul, S.st.shape[ne][0], S.st.shape[ne][1]);
+      T v = factored_rt<T, MQ, ML>(xe, R.vq, R.vl, S.st.shape[ne][2], S.st.shape[ne][3]);
+      T w = A::div(u, v);
+      T h = A::mul(R.q2, w);
+      h = A::fma(h, xe, R.q1);
+      T Q = A::fma(h, xe, R.q0);
+      T sq = A::sqrt(Q);
+      T s = ne == 0 ? sq : A::mul(powi_rt(Q, ne), sq);
+      S.sy[e] = A::fma(s, S.stt[e], xe);
+    }
+    if (in) S.perm[S.hist[n] + rank_in_bin] = (short)tid;
+    __syncthreads();
+    // phase B: order-sorted tails
+    const int cntE = (int)(last - i0);
+    const bool has = tid < cntE;
+    const int e = has ? S.perm[tid] : 0;
+    const int ne = has ? S.sn[e] : 0;
+    unsigned todo = __ballot_sync(0xffffffffu, has);
+    while (todo) {
+      const int nl = __shfl_sync(0xffffffffu, ne, __ffs(todo) - 1);
+      const bool mine = has && ne == nl;
+      const unsigned mask = __ballot_sync(0xffffffffu, mine);
+      if (mine)
+        tail_dispatch<T, NB>(nl, S.sx[e], S.sy[e], S.stt[e], S.sok[e] != 0, mask,
+                             S.obuf + S.soff[e]);
+      todo &= ~mask;
     }
     __syncthreads();
     T* dst = out + base;
-    for (int64_t k = tid; k < cnt; k += kThreads) __stcs(dst + k, obuf[k]);
+    for (int k = tid; k < (int)cnt; k += kThreads) __stcs(dst + k, S.obuf[k]);
   }
 }
 
@@ -496,8 +645,15 @@ static boys_status launch_ragged(const void* x, const uint8_t* nm, const int64_t
                                  void* out, int64_t* dom, cudaStream_t s) {
   constexpr int NB = Tab<T>::MAX_ORDER;
   auto k = ragged_kernel<T, NB>;
+  const size_t smem = sizeof(RaggedSmem<T, NB>);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return cuda_status(e);
+    attr = true;
+  }
   int64_t ntiles = (N + kThreads - 1) / kThreads;
-  k<<<blocks_for(k, 0, ntiles), kThreads, 0, s>>>((const T*)x, nm, off, N, (T*)out, dom);
+  k<<<blocks_for(k, smem, ntiles), kThreads, smem, s>>>((const T*)x, nm, off, N, (T*)out, dom);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cuda_status(cudaGetLastError());
 }
