@@ -454,7 +454,8 @@ def main():
 
     # end-to-end (host buffers through the C-ABI), rank-local then summed
     try:
-        e2e = e2e_dense(args.config, args.e2e_steps, dev) if cfg.layout != "ragged" else None
+        e2e = (e2e_dense(args.config, args.e2e_steps, dev)
+               if cfg.layout != "ragged" and args.e2e_steps > 0 else None)
         if e2e:
             e2e["value"] = sum_over_ranks(e2e["value"], ws)
         line["e2e"] = e2e
@@ -462,7 +463,7 @@ def main():
         line["e2e"] = {"error": str(ex)[:200]}
 
     # CPU baseline: the C oracle on the host cores, rank 0 at N=1 only
-    if rank == 0 and ws == 1 and cfg.layout != "ragged":
+    if rank == 0 and ws == 1 and cfg.layout != "ragged" and args.cpu_seconds > 0:
         xs = wl.xs[0][: 1 << 21].cpu().numpy()
         v, cores, reps = cpu_port_rate(cfg.n_max, xs, cfg.layout, args.cpu_seconds)
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",

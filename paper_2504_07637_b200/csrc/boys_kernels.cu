@@ -15,6 +15,7 @@
 
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -95,22 +96,46 @@ __device__ __forceinline__ void eval_point(T x_in, bool ok, T (&Fv)[n + 1], T& t
 
 // ---------------------------------------------------------------------------
 // dense kernel
+//
+// Persistent grid over 256-point tiles, one point per thread, x of the next
+// tile prefetched into registers while the current one computes.
+// SoA: coalesced streaming stores per order row.
+// AoS: each warp stages its 32 rows ([32][n+1], contiguous in global memory)
+//      in its own shared-memory slot and issues its own bulk async copy
+//      (TMA engine) -- no block-wide barrier; NBUF slots per warp rotate so
+//      the copy of one tile overlaps the computation of the next.
 // ---------------------------------------------------------------------------
-template <typename T, int n, bool AOS>
-__global__ void __launch_bounds__(kThreads)
+enum : int { kPrefetch = 1, kWarpStore = 2 };
+
+template <typename T, int n, bool AOS, int NBUF>
+__global__ void __launch_bounds__(kThreads, (n <= 1 && !AOS) ? 8 : 4)
 dense_kernel(const T* __restrict__ X, int64_t N, T* __restrict__ out, T* __restrict__ expx,
-             int64_t* __restrict__ dom, int64_t index_base, bool bulk_ok) {
+             int64_t* __restrict__ dom, int64_t index_base, bool bulk_ok, int flags) {
   constexpr int W = n + 1;
+  constexpr int WARP_ELEMS = 32 * W;           // one warp's rows
+  constexpr int TILE_ELEMS = kThreads * W;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  T* bufs = reinterpret_cast<T*>(smem_raw);   // AoS: 2 x [kThreads][W]
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool prefetch = flags & kPrefetch;
+  const bool warp_store = flags & kWarpStore;
+  T* sbase = reinterpret_cast<T*>(smem_raw);
   const int64_t ntiles = (N + kThreads - 1) / kThreads;
+  int64_t tile = blockIdx.x;
+  T x_next = T(0);
+  if (prefetch && tile < ntiles && tile * kThreads + tid < N) x_next = ldg_nc(X + tile * kThreads + tid);
   int it = 0;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+  for (; tile < ntiles; tile += gridDim.x, ++it) {
     const int64_t i0 = tile * kThreads;
     const int64_t i = i0 + tid;
     const bool in = i < N;
-    T x = in ? ldg_nc(X + i) : T(0);
+    T x;
+    if (prefetch) {
+      x = x_next;
+      const int64_t inx = i + (int64_t)gridDim.x * kThreads;
+      if (tile + gridDim.x < ntiles && inx < N) x_next = ldg_nc(X + inx);
+    } else {
+      x = in ? ldg_nc(X + i) : T(0);
+    }
     bool ok = valid_x(x);
     if (in && !ok) flag_domain(dom, index_base + i);
     ok = ok || !in;   // tail lanes evaluate x = 0 quietly
@@ -123,10 +148,34 @@ dense_kernel(const T* __restrict__ X, int64_t N, T* __restrict__ out, T* __restr
 #pragma unroll
         for (int m = 0; m < W; ++m) __stcs(out + (int64_t)m * N + i, Fv[m]);
       }
+    } else if (warp_store) {
+      // per-warp slot, per-warp bulk copy, no block barrier
+      T* buf = sbase + warp * (NBUF * WARP_ELEMS) + (it % NBUF) * WARP_ELEMS;
+      if (lane == 0) {
+        if constexpr (NBUF == 1) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+        else asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+      }
+      __syncwarp();
+#pragma unroll
+      for (int m = 0; m < W; ++m) buf[lane * W + m] = Fv[m];
+      const int64_t w0 = i0 + warp * 32;
+      const int64_t rows = N - w0 < 32 ? (N - w0 > 0 ? N - w0 : 0) : 32;
+      if (bulk_ok && rows == 32) {
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) bulk_store(out + w0 * W, buf, WARP_ELEMS * sizeof(T));
+      } else {
+        __syncwarp();
+        T* dst = out + w0 * W;
+        for (int k = lane; k < rows * W; k += 32) __stcs(dst + k, buf[k]);
+      }
     } else {
-      T* buf = bufs + (it & 1) * (kThreads * W);
-      // buffer (it&1) was handed to the bulk engine two tiles ago: wait until read
-      if (tid == 0) bulk_wait_read_le1();
+      // block-wide tile, one bulk copy per tile
+      T* buf = sbase + (it % NBUF) * TILE_ELEMS;
+      if (tid == 0) {
+        if constexpr (NBUF == 1) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+        else asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+      }
       __syncthreads();
 #pragma unroll
       for (int m = 0; m < W; ++m) buf[tid * W + m] = Fv[m];
@@ -134,7 +183,7 @@ dense_kernel(const T* __restrict__ X, int64_t N, T* __restrict__ out, T* __restr
       if (bulk_ok && cnt == kThreads) {
         fence_proxy_async_smem();
         __syncthreads();
-        if (tid == 0) bulk_store(out + i0 * W, buf, kThreads * W * sizeof(T));
+        if (tid == 0) bulk_store(out + i0 * W, buf, TILE_ELEMS * sizeof(T));
       } else {
         __syncthreads();
         T* dst = out + i0 * W;
@@ -143,7 +192,7 @@ dense_kernel(const T* __restrict__ X, int64_t N, T* __restrict__ out, T* __restr
     }
   }
   if constexpr (AOS) {
-    if (tid == 0) bulk_wait_all();
+    if ((warp_store && lane == 0) || tid == 0) bulk_wait_all();
   }
 }
 
@@ -278,6 +327,55 @@ __device__ __forceinline__ void eval_point_rt(T x_in, bool ok, int n, const Smem
 // Every value is bit-identical to boys_eval_dense at the element's order.
 // Tiles holding an order above the table fall back to direct NaN writes.
 // ---------------------------------------------------------------------------
+// ragged v1: every lane runs the run-time-order evaluator (exact select
+// predication to the compile-time bound NB); kept for A/B measurement.
+template <typename T, int NB>
+__global__ void __launch_bounds__(kThreads)
+ragged_v1_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
+                 const int64_t* __restrict__ OFF, int64_t N, T* __restrict__ out,
+                 int64_t* __restrict__ dom) {
+  using A = Ar<T>;
+  constexpr int MQ = MaxShape<T>::Q(), ML = MaxShape<T>::L();
+  __shared__ SmemTable<T> st;
+  __shared__ T obuf[kThreads * (NB + 1)];
+  stage_table(st);
+  __syncthreads();
+  const int tid = threadIdx.x;
+  const int64_t ntiles = (N + kThreads - 1) / kThreads;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t i0 = tile * kThreads;
+    const int64_t i = i0 + tid;
+    const bool in = i < N;
+    const int64_t last = (i0 + kThreads < N) ? i0 + kThreads : N;
+    const int64_t base = OFF[i0];
+    const int64_t cnt = OFF[last] - base;
+    T x = in ? ldg_nc(X + i) : T(0);
+    const int n = in ? (int)NM[i] : 0;
+    const int64_t off = in ? OFF[i] - base : 0;
+    const bool xok = valid_x(x);
+    if (in && !(xok && n <= NB)) flag_domain(dom, i);
+    T Fv[NB + 1];
+    T t;
+    eval_point_rt<T, NB, MQ, ML>(x, xok || !in, n <= NB ? n : 0, st, Fv, t);
+    const bool bad_tile = __syncthreads_or(in && n > NB);   // also: obuf free
+    if (bad_tile) {
+      if (in) {
+        T* dst = out + base + off;
+        for (int m = 0; m <= n; ++m) dst[m] = (n > NB || !xok) ? A::nan() : Fv[m <= NB ? m : NB];
+      }
+      continue;
+    }
+    if (in) {
+#pragma unroll
+      for (int m = 0; m <= NB; ++m)
+        if (m <= n) obuf[off + m] = Fv[m];
+    }
+    __syncthreads();
+    T* dst = out + base;
+    for (int64_t k = tid; k < cnt; k += kThreads) __stcs(dst + k, obuf[k]);
+  }
+}
+
 template <typename T, int NB>
 struct RaggedSmem {
   SmemTable<T> st;
@@ -562,21 +660,44 @@ static boys_status cuda_status(cudaError_t e) {
   return BOYS_E_CUDA;
 }
 
+// Persistent grid (SMs x resident blocks) for large batches; for small ones
+// (<= 4 waves) one block per tile so the block scheduler balances the tail.
 template <typename K>
 static int blocks_for(K kernel, size_t smem, int64_t ntiles) {
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, smem);
   if (occ < 1) occ = 1;
   int64_t b = (int64_t)sm_count() * occ;
-  if (ntiles < b) b = ntiles;
+  if (ntiles <= 4 * b) b = ntiles;
   return (int)(b < 1 ? 1 : b);
 }
 
-template <typename T, int n, bool AOS>
-static boys_status launch_dense_t(const T* x, int64_t N, T* out, T* expx, int64_t* dom,
+// Tuning knobs (read once; defaults are the measured best on B200):
+//   BOYS_AOS_NBUF    staging depth (1 or 2)
+//   BOYS_DENSE_FLAGS bit0 prefetch next tile's x, bit1 per-warp bulk stores
+//   BOYS_RAGGED_V    ragged kernel variant (1 = predicated, 2 = compacted/sorted)
+static int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+static int aos_nbuf() {
+  static int v = env_int("BOYS_AOS_NBUF", 2) == 1 ? 1 : 2;
+  return v;
+}
+static int dense_flags() {
+  static int v = env_int("BOYS_DENSE_FLAGS", 0);
+  return v;
+}
+static int ragged_variant() {
+  static int v = env_int("BOYS_RAGGED_V", 2);
+  return v;
+}
+
+template <typename T, int n, bool AOS, int NBUF>
+static boys_status launch_dense_k(const T* x, int64_t N, T* out, T* expx, int64_t* dom,
                                   int64_t base, cudaStream_t s) {
-  auto k = dense_kernel<T, n, AOS>;
-  size_t smem = AOS ? 2 * kThreads * (n + 1) * sizeof(T) : 0;
+  auto k = dense_kernel<T, n, AOS, NBUF>;
+  size_t smem = AOS ? (size_t)NBUF * kThreads * (n + 1) * sizeof(T) : 0;
   static bool attr = false;   // per instantiation
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -585,9 +706,17 @@ static boys_status launch_dense_t(const T* x, int64_t N, T* out, T* expx, int64_
   }
   int64_t ntiles = (N + kThreads - 1) / kThreads;
   bool bulk_ok = (reinterpret_cast<uintptr_t>(out) % 16) == 0;
-  k<<<blocks_for(k, smem, ntiles), kThreads, smem, s>>>(x, N, out, expx, dom, base, bulk_ok);
+  k<<<blocks_for(k, smem, ntiles), kThreads, smem, s>>>(x, N, out, expx, dom, base, bulk_ok,
+                                                        dense_flags());
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cuda_status(cudaGetLastError());
+}
+
+template <typename T, int n, bool AOS>
+static boys_status launch_dense_t(const T* x, int64_t N, T* out, T* expx, int64_t* dom,
+                                  int64_t base, cudaStream_t s) {
+  if (AOS && aos_nbuf() == 1) return launch_dense_k<T, n, AOS, 1>(x, N, out, expx, dom, base, s);
+  return launch_dense_k<T, n, AOS, 2>(x, N, out, expx, dom, base, s);
 }
 
 template <typename T, int n>
@@ -644,16 +773,21 @@ template <typename T>
 static boys_status launch_ragged(const void* x, const uint8_t* nm, const int64_t* off, int64_t N,
                                  void* out, int64_t* dom, cudaStream_t s) {
   constexpr int NB = Tab<T>::MAX_ORDER;
-  auto k = ragged_kernel<T, NB>;
-  const size_t smem = sizeof(RaggedSmem<T, NB>);
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return cuda_status(e);
-    attr = true;
-  }
   int64_t ntiles = (N + kThreads - 1) / kThreads;
-  k<<<blocks_for(k, smem, ntiles), kThreads, smem, s>>>((const T*)x, nm, off, N, (T*)out, dom);
+  if (ragged_variant() == 1) {
+    auto k = ragged_v1_kernel<T, NB>;
+    k<<<blocks_for(k, 0, ntiles), kThreads, 0, s>>>((const T*)x, nm, off, N, (T*)out, dom);
+  } else {
+    auto k = ragged_kernel<T, NB>;
+    const size_t smem = sizeof(RaggedSmem<T, NB>);
+    static bool attr = false;
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return cuda_status(e);
+      attr = true;
+    }
+    k<<<blocks_for(k, smem, ntiles), kThreads, smem, s>>>((const T*)x, nm, off, N, (T*)out, dom);
+  }
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cuda_status(cudaGetLastError());
 }
