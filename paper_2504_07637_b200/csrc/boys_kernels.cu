@@ -1,16 +1,20 @@
 // sm_100a kernels and the C ABI of libboys (include/boys.h).
 //
-// dense  : persistent grid, one point per thread, 256-point tiles.
-//          SoA  -> coalesced streaming stores, one row per order.
-//          AoS  -> [256][n+1] tile staged in shared memory (odd row stride =>
-//                  conflict-free 64-bit banks), then ONE bulk async copy
-//                  (cp.async.bulk.global.shared::cta, TMA engine) per tile,
-//                  double-buffered so the next tile computes while the
-//                  previous one drains to HBM.
-// ragged : per-element order; tables staged in shared memory, run-time-order
-//          evaluator with exact select predication (bit-identical to dense),
-//          output staged per block and written with coalesced stores.
+// dense  : persistent grid of 256-point tiles, one point per thread; each
+//          F_m is streamed to its destination as the recursion produces it
+//          (no per-thread value array).
+//          SoA -> coalesced streaming stores, one row per order.
+//          AoS -> the [256][n+1] tile is staged in shared memory (odd row
+//                 stride => conflict-free 64-bit banks) and leaves as ONE bulk
+//                 async copy (cp.async.bulk.global.shared::cta, TMA engine)
+//                 that overlaps the next tile's computation.
+// ragged : per-element order.  Per tile: ballot-compact the elements needing
+//          e^{-x} (x <= XEXP) and Q~ (x < z_{n_i}) into one work list (phase
+//          A); then every lane runs the cheap run-time-order tail for its own
+//          element, recursion bounded by the warp's largest order (phase B);
+//          output staged per tile, written with coalesced stores.
 // split  : eval_with_split (two seeds, two recursions).
+// All values are bit-identical to the CPU oracle (oracle/boys_oracle.c).
 #include <cuda_runtime.h>
 
 #include <atomic>
@@ -24,12 +28,13 @@
 #include "boys_eval.cuh"
 
 #ifndef BOYS_VERSION
-#define BOYS_VERSION "0.1.0"
+#define BOYS_VERSION "0.2.0"
 #endif
 
 namespace boys {
 
 constexpr int kThreads = 256;   // points per tile == threads per block
+constexpr unsigned kFull = 0xffffffffu;
 
 static std::atomic<int64_t> g_launches{0};
 static thread_local char g_cuda_err[256] = "";
@@ -49,8 +54,9 @@ __device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, uint32_
                : "memory");
   asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
 }
-__device__ __forceinline__ void bulk_wait_read_le1() {
-  asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+template <int PENDING>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;\n" ::"n"(PENDING) : "memory");
 }
 __device__ __forceinline__ void bulk_wait_all() {
   asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
@@ -61,124 +67,82 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 
 template <typename T> __device__ __forceinline__ T ldg_nc(const T* p) { return __ldg(p); }
 
-// F_0..F_n for one point into Fv[]; returns false if x is outside the domain.
-// `ok` lanes only influence warp-uniform shortcuts, never values.
-template <typename T, int n>
-__device__ __forceinline__ void eval_point(T x_in, bool ok, T (&Fv)[n + 1], T& t_out) {
+// F_0..F_n for one point, handed to put(m, value) in the order n, n-1, .., 0
+// (then, for lanes past x_up, 0..n again with the upward values).  Returns
+// e^{-x}.  `ok` = x in the domain; other lanes produce NaN.  Lanes only
+// influence warp-uniform shortcuts (skip Q~ / the upward ladder), never values.
+template <typename T, int n, typename Put>
+__device__ __forceinline__ T eval_point_stream(T x_in, bool ok, Put&& put) {
   using A = Ar<T>;
   const BoysRow<T>& R = Tab<T>::row(n);
+  const T bad = A::nan();
   T x = ok ? x_in : T(0);
   T t = exp_neg_clamped(x);
-  bool below = ok && x < R.z;
-  bool any_below = __any_sync(0xffffffffu, below);
-  Fv[n] = seed<T, n>(x, t, any_below);
+  bool any_below = __any_sync(kFull, ok && x < R.z);
+  T cur = seed<T, n>(x, t, any_below);
+  put(n, ok ? cur : bad);
   T tx = A::add(x, x);
 #pragma unroll
-  for (int m = n - 1; m >= 0; --m) Fv[m] = A::mul(A::fma(tx, Fv[m + 1], t), rinv<T>(m));
+  for (int m = n - 1; m >= 0; --m) {
+    cur = A::mul(A::fma(tx, cur, t), rinv<T>(m));
+    put(m, ok ? cur : bad);
+  }
   bool up = ok && x > R.x_up;
-  if (__any_sync(0xffffffffu, up)) {
+  if (__any_sync(kFull, up)) {
     T rx = A::rcp(x);
     T f = up_first(x);
-    Fv[0] = up ? f : Fv[0];
+    if (up) put(0, f);
 #pragma unroll
     for (int m = 0; m < n; ++m) {
       f = up_next(f, m, rx);
-      Fv[m + 1] = up ? f : Fv[m + 1];
+      if (up) put(m + 1, f);
     }
   }
-  if (!ok) {
-#pragma unroll
-    for (int m = 0; m <= n; ++m) Fv[m] = A::nan();
-    t = A::nan();
-  }
-  t_out = t;
+  return ok ? t : bad;
+}
+
+// Array form (split kernel).
+template <typename T, int n>
+__device__ __forceinline__ void eval_point(T x_in, bool ok, T (&Fv)[n + 1], T& t_out) {
+  t_out = eval_point_stream<T, n>(x_in, ok, [&](int m, T v) { Fv[m] = v; });
 }
 
 // ---------------------------------------------------------------------------
 // dense kernel
-//
-// Persistent grid over 256-point tiles, one point per thread, x of the next
-// tile prefetched into registers while the current one computes.
-// SoA: coalesced streaming stores per order row.
-// AoS: each warp stages its 32 rows ([32][n+1], contiguous in global memory)
-//      in its own shared-memory slot and issues its own bulk async copy
-//      (TMA engine) -- no block-wide barrier; NBUF slots per warp rotate so
-//      the copy of one tile overlaps the computation of the next.
 // ---------------------------------------------------------------------------
-enum : int { kPrefetch = 1, kWarpStore = 2 };
-
-template <typename T, int n, bool AOS, int NBUF>
-__global__ void __launch_bounds__(kThreads, (n <= 1 && !AOS) ? 8 : 4)
+template <typename T, int n, bool AOS, int NBUF, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
 dense_kernel(const T* __restrict__ X, int64_t N, T* __restrict__ out, T* __restrict__ expx,
-             int64_t* __restrict__ dom, int64_t index_base, bool bulk_ok, int flags) {
+             int64_t* __restrict__ dom, int64_t index_base, bool bulk_ok) {
   constexpr int W = n + 1;
-  constexpr int WARP_ELEMS = 32 * W;           // one warp's rows
   constexpr int TILE_ELEMS = kThreads * W;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const bool prefetch = flags & kPrefetch;
-  const bool warp_store = flags & kWarpStore;
   T* sbase = reinterpret_cast<T*>(smem_raw);
+  const int tid = threadIdx.x;
   const int64_t ntiles = (N + kThreads - 1) / kThreads;
-  int64_t tile = blockIdx.x;
-  T x_next = T(0);
-  if (prefetch && tile < ntiles && tile * kThreads + tid < N) x_next = ldg_nc(X + tile * kThreads + tid);
   int it = 0;
-  for (; tile < ntiles; tile += gridDim.x, ++it) {
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
     const int64_t i0 = tile * kThreads;
     const int64_t i = i0 + tid;
     const bool in = i < N;
-    T x;
-    if (prefetch) {
-      x = x_next;
-      const int64_t inx = i + (int64_t)gridDim.x * kThreads;
-      if (tile + gridDim.x < ntiles && inx < N) x_next = ldg_nc(X + inx);
-    } else {
-      x = in ? ldg_nc(X + i) : T(0);
-    }
+    const T x = in ? ldg_nc(X + i) : T(0);
     bool ok = valid_x(x);
     if (in && !ok) flag_domain(dom, index_base + i);
     ok = ok || !in;   // tail lanes evaluate x = 0 quietly
-    T Fv[W];
-    T t;
-    eval_point<T, n>(in ? x : T(0), ok, Fv, t);
-    if (expx && in) __stcs(expx + i, t);
     if constexpr (!AOS) {
-      if (in) {
-#pragma unroll
-        for (int m = 0; m < W; ++m) __stcs(out + (int64_t)m * N + i, Fv[m]);
-      }
-    } else if (warp_store) {
-      // per-warp slot, per-warp bulk copy, no block barrier
-      T* buf = sbase + warp * (NBUF * WARP_ELEMS) + (it % NBUF) * WARP_ELEMS;
-      if (lane == 0) {
-        if constexpr (NBUF == 1) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
-        else asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
-      }
-      __syncwarp();
-#pragma unroll
-      for (int m = 0; m < W; ++m) buf[lane * W + m] = Fv[m];
-      const int64_t w0 = i0 + warp * 32;
-      const int64_t rows = N - w0 < 32 ? (N - w0 > 0 ? N - w0 : 0) : 32;
-      if (bulk_ok && rows == 32) {
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) bulk_store(out + w0 * W, buf, WARP_ELEMS * sizeof(T));
-      } else {
-        __syncwarp();
-        T* dst = out + w0 * W;
-        for (int k = lane; k < rows * W; k += 32) __stcs(dst + k, buf[k]);
-      }
+      T* o = out + i;
+      T t = eval_point_stream<T, n>(x, ok, [&](int m, T v) {
+        if (in) __stcs(o + (int64_t)m * N, v);
+      });
+      if (expx && in) __stcs(expx + i, t);
     } else {
-      // block-wide tile, one bulk copy per tile
       T* buf = sbase + (it % NBUF) * TILE_ELEMS;
-      if (tid == 0) {
-        if constexpr (NBUF == 1) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
-        else asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
-      }
+      // the slot went to the bulk engine NBUF tiles ago: wait until it was read
+      if (tid == 0) bulk_wait_read<NBUF - 1>();
       __syncthreads();
-#pragma unroll
-      for (int m = 0; m < W; ++m) buf[tid * W + m] = Fv[m];
+      T* row = buf + tid * W;
+      T t = eval_point_stream<T, n>(x, ok, [&](int m, T v) { row[m] = v; });
+      if (expx && in) __stcs(expx + i, t);
       const int64_t cnt = (N - i0) < kThreads ? (N - i0) : kThreads;
       if (bulk_ok && cnt == kThreads) {
         fence_proxy_async_smem();
@@ -192,7 +156,7 @@ dense_kernel(const T* __restrict__ X, int64_t N, T* __restrict__ out, T* __restr
     }
   }
   if constexpr (AOS) {
-    if ((warp_store && lane == 0) || tid == 0) bulk_wait_all();
+    if (tid == 0) bulk_wait_all();
   }
 }
 
@@ -213,29 +177,6 @@ __device__ __forceinline__ void stage_table(SmemTable<T>& st) {
   for (int k = threadIdx.x; k < words; k += blockDim.x) dst[k] = src[k];
   for (int k = threadIdx.x; k < (Tab<T>::MAX_ORDER + 1) * 4; k += blockDim.x)
     (&st.shape[0][0])[k] = Tab<T>::shape(k / 4, k % 4);
-}
-
-// Seed F_n(x) for a run-time order n; identical operation sequence to seed<T,n>.
-template <typename T, int MQ, int ML>
-__device__ __forceinline__ T seed_rt(T x, T t, int n, const SmemTable<T>& st, bool any_below) {
-  using A = Ar<T>;
-  const BoysRow<T>& R = st.row[n];
-  T y = x;
-  if (any_below) {
-    T u = factored_rt<T, MQ, ML>(x, R.uq, R.ul, st.shape[n][0], st.shape[n][1]);
-    T v = factored_rt<T, MQ, ML>(x, R.vq, R.vl, st.shape[n][2], st.shape[n][3]);
-    T w = A::div(u, v);
-    T h = A::mul(R.q2, w);
-    h = A::fma(h, x, R.q1);
-    T Q = A::fma(h, x, R.q0);
-    T sq = A::sqrt(Q);
-    T s = n == 0 ? sq : A::mul(powi_rt(Q, n), sq);
-    T yq = A::fma(s, t, x);
-    y = x < R.z ? yq : x;
-  }
-  T r = A::rcp(y);
-  T sr = A::sqrt(r);
-  return n == 0 ? A::mul(R.c, sr) : A::mul(A::mul(R.c, powi_rt(r, n)), sr);
 }
 
 template <typename T> struct MaxShape;   // compile-time bounds on factor counts
@@ -268,163 +209,107 @@ template <> struct MaxShape<float> {
   }
 };
 
-// Run-time order evaluation of F_0..F_n into Fv[0..n] (entries above n are
-// unspecified).  Operation-for-operation the same as eval_point<T, n>.
-template <typename T, int NB, int MQ, int ML>
+// y = x + Q~^{n+1/2} e^{-x} below the cut-off, run-time order; identical
+// operation sequence to seed<T, n>'s Q~ branch.
+template <typename T>
+__device__ __forceinline__ T y_below_rt(T x, T t, int n, const SmemTable<T>& st) {
+  using A = Ar<T>;
+  constexpr int MQ = MaxShape<T>::Q(), ML = MaxShape<T>::L();
+  const BoysRow<T>& R = st.row[n];
+  T u = factored_rt<T, MQ, ML>(x, R.uq, R.ul, st.shape[n][0], st.shape[n][1]);
+  T v = factored_rt<T, MQ, ML>(x, R.vq, R.vl, st.shape[n][2], st.shape[n][3]);
+  T w = A::div(u, v);
+  T h = A::mul(R.q2, w);
+  h = A::fma(h, x, R.q1);
+  T Q = A::fma(h, x, R.q0);
+  T sq = A::sqrt(Q);
+  T s = n == 0 ? sq : A::mul(powi_rt(Q, n), sq);
+  return A::fma(s, t, x);
+}
+
+// b^n for n < 2^bits (bits: warp-uniform bound); same products as powi<T,n>.
+template <typename T>
+__device__ __forceinline__ T powi_rt_bounded(T b, int n, int bits) {
+  using A = Ar<T>;
+  T r = b, p = b;
+  bool have = false;
+#pragma unroll
+  for (int j = 0; j < 6; ++j) {
+    if (j >= bits) break;
+    bool bit = (n >> j) & 1;
+    T rr = have ? A::mul(r, p) : p;
+    r = bit ? rr : r;
+    have = have || bit;
+    if ((n >> (j + 1)) != 0) p = A::mul(p, p);
+  }
+  return r;
+}
+
+// Tail for a run-time order n (per lane): F_n from y, then the recursion and
+// the upward ladder, handed to put(m, v).  `wmax` = warp-uniform max order.
+template <typename T, int NB, typename Put>
+__device__ __forceinline__ void tail_rt(T x, T y, T t, int n, bool ok, int wmax,
+                                        const SmemTable<T>& st, Put&& put) {
+  using A = Ar<T>;
+  const T bad = A::nan();
+  const int bits = 32 - __clz(wmax | 1);
+  T r = A::rcp(y);
+  T sr = A::sqrt(r);
+  const T c = st.row[n].c;
+  T cur = n == 0 ? A::mul(c, sr) : A::mul(A::mul(c, powi_rt_bounded(r, n, bits)), sr);
+  put(n, ok ? cur : bad);
+  T tx = A::add(x, x);
+#pragma unroll
+  for (int m = NB - 1; m >= 0; --m) {
+    if (m >= wmax) continue;                       // warp-uniform
+    if (m < n) {
+      cur = A::mul(A::fma(tx, cur, t), rinv<T>(m));
+      put(m, ok ? cur : bad);
+    }
+  }
+  bool up = ok && x > st.row[n].x_up;
+  if (__any_sync(kFull, up)) {
+    T rx = A::rcp(x);
+    T f = up_first(x);
+    if (up) put(0, f);
+#pragma unroll
+    for (int m = 0; m < NB; ++m) {
+      if (m >= wmax) break;
+      f = up_next(f, m, rx);
+      if (up && m + 1 <= n) put(m + 1, f);
+    }
+  }
+}
+
+// Complete run-time-order evaluation (split kernel; ragged fallback tiles).
+template <typename T, int NB, typename Put>
 __device__ __forceinline__ void eval_point_rt(T x_in, bool ok, int n, const SmemTable<T>& st,
-                                              T (&Fv)[NB + 1], T& t_out) {
+                                              Put&& put) {
   using A = Ar<T>;
   T x = ok ? x_in : T(0);
   int ns = ok ? n : 0;
   T t = exp_neg_clamped(x);
   bool below = ok && x < st.row[ns].z;
-  bool any_below = __any_sync(0xffffffffu, below);
-  T cur = seed_rt<T, MQ, ML>(x, t, ns, st, any_below);
-  Fv[NB] = cur;
-  T tx = A::add(x, x);
-#pragma unroll
-  for (int m = NB - 1; m >= 0; --m) {
-    T nx = A::mul(A::fma(tx, cur, t), rinv<T>(m));
-    cur = m < ns ? nx : cur;
-    Fv[m] = cur;
+  T y = x;
+  if (__any_sync(kFull, below)) {
+    T yq = y_below_rt(x, t, ns, st);
+    y = below ? yq : x;
   }
-  bool up = ok && x > st.row[ns].x_up;
-  if (__any_sync(0xffffffffu, up)) {
-    T rx = A::rcp(x);
-    T f = up_first(x);
-    Fv[0] = up ? f : Fv[0];
-#pragma unroll
-    for (int m = 0; m < NB; ++m) {
-      f = up_next(f, m, rx);
-      Fv[m + 1] = (up && m + 1 <= ns) ? f : Fv[m + 1];
-    }
-  }
-  if (!ok) {
-#pragma unroll
-    for (int m = 0; m <= NB; ++m) Fv[m] = A::nan();
-    t = A::nan();
-  }
-  t_out = t;
+  int wmax = __reduce_max_sync(kFull, (unsigned)ns);
+  tail_rt<T, NB>(x, y, t, ns, ok, wmax, st, put);
 }
 
 // ---------------------------------------------------------------------------
 // ragged kernel: element i, order n_i, values at out[offsets[i] + m]
-//
-// Per 256-element tile:
-//   stage    x, n, local output offset into shared memory; ballot-compact the
-//            elements that need e^{-x} (x <= XEXP) and those below their
-//            cut-off (x < z_{n_i}) into two lists; counting-sort the tile by
-//            order n_i.
-//   phase A  threads sweep the compacted lists: e^{-x}, then Q~ / s / y with
-//            the run-time-order evaluator (per-lane tables from shared memory)
-//            -- only ~28% / ~5% of ERI-like elements pay for these.
-//   phase B  each thread takes one element of the order-sorted tile; a warp
-//            loops over the (usually one or two) distinct orders it holds and
-//            runs the compile-time-order tail (r = 1/y, F_n, recursion,
-//            upward ladder) for that order, writing into the staged tile.
-//   store    the tile's contiguous output range leaves with coalesced
-//            streaming stores.
-// Every value is bit-identical to boys_eval_dense at the element's order.
-// Tiles holding an order above the table fall back to direct NaN writes.
 // ---------------------------------------------------------------------------
-// ragged v1: every lane runs the run-time-order evaluator (exact select
-// predication to the compile-time bound NB); kept for A/B measurement.
-template <typename T, int NB>
-__global__ void __launch_bounds__(kThreads)
-ragged_v1_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
-                 const int64_t* __restrict__ OFF, int64_t N, T* __restrict__ out,
-                 int64_t* __restrict__ dom) {
-  using A = Ar<T>;
-  constexpr int MQ = MaxShape<T>::Q(), ML = MaxShape<T>::L();
-  __shared__ SmemTable<T> st;
-  __shared__ T obuf[kThreads * (NB + 1)];
-  stage_table(st);
-  __syncthreads();
-  const int tid = threadIdx.x;
-  const int64_t ntiles = (N + kThreads - 1) / kThreads;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t i0 = tile * kThreads;
-    const int64_t i = i0 + tid;
-    const bool in = i < N;
-    const int64_t last = (i0 + kThreads < N) ? i0 + kThreads : N;
-    const int64_t base = OFF[i0];
-    const int64_t cnt = OFF[last] - base;
-    T x = in ? ldg_nc(X + i) : T(0);
-    const int n = in ? (int)NM[i] : 0;
-    const int64_t off = in ? OFF[i] - base : 0;
-    const bool xok = valid_x(x);
-    if (in && !(xok && n <= NB)) flag_domain(dom, i);
-    T Fv[NB + 1];
-    T t;
-    eval_point_rt<T, NB, MQ, ML>(x, xok || !in, n <= NB ? n : 0, st, Fv, t);
-    const bool bad_tile = __syncthreads_or(in && n > NB);   // also: obuf free
-    if (bad_tile) {
-      if (in) {
-        T* dst = out + base + off;
-        for (int m = 0; m <= n; ++m) dst[m] = (n > NB || !xok) ? A::nan() : Fv[m <= NB ? m : NB];
-      }
-      continue;
-    }
-    if (in) {
-#pragma unroll
-      for (int m = 0; m <= NB; ++m)
-        if (m <= n) obuf[off + m] = Fv[m];
-    }
-    __syncthreads();
-    T* dst = out + base;
-    for (int64_t k = tid; k < cnt; k += kThreads) __stcs(dst + k, obuf[k]);
-  }
-}
-
 template <typename T, int NB>
 struct RaggedSmem {
   SmemTable<T> st;
   T obuf[kThreads * (NB + 1)];
   T sx[kThreads], sy[kThreads], stt[kThreads];
-  int soff[kThreads];
-  int hist[NB + 2];
-  short perm[kThreads];
-  short listE[kThreads], listQ[kThreads];
-  unsigned char sn[kThreads], sok[kThreads];
-  int nE, nQ;
+  short listQ[kThreads], listE[kThreads];
+  int nQ, nE;
 };
-
-// F_n from y (= x past the cut-off) and the recursion/upward ladder, written
-// to dst[0..n].  `mask` = lanes of this warp holding order n.
-template <typename T, int n>
-__device__ __forceinline__ void tail_store(T x, T y, T t, bool ok, unsigned mask, T* dst) {
-  using A = Ar<T>;
-  const BoysRow<T>& R = Tab<T>::row(n);
-  T Fv[n + 1];
-  T r = A::rcp(y);
-  T sr = A::sqrt(r);
-  Fv[n] = n == 0 ? A::mul(R.c, sr) : A::mul(A::mul(R.c, powi<T, (n == 0 ? 1 : n)>(r)), sr);
-  T tx = A::add(x, x);
-#pragma unroll
-  for (int m = n - 1; m >= 0; --m) Fv[m] = A::mul(A::fma(tx, Fv[m + 1], t), rinv<T>(m));
-  bool up = ok && x > R.x_up;
-  if (__any_sync(mask, up)) {
-    T rx = A::rcp(x);
-    T f = up_first(x);
-    Fv[0] = up ? f : Fv[0];
-#pragma unroll
-    for (int m = 0; m < n; ++m) {
-      f = up_next(f, m, rx);
-      Fv[m + 1] = up ? f : Fv[m + 1];
-    }
-  }
-#pragma unroll
-  for (int m = 0; m <= n; ++m) dst[m] = ok ? Fv[m] : A::nan();
-}
-
-template <typename T, int NB, int n = 0>
-__device__ __forceinline__ void tail_dispatch(int nn, T x, T y, T t, bool ok, unsigned mask,
-                                              T* dst) {
-  if constexpr (n <= NB) {
-    if (nn == n) tail_store<T, n>(x, y, t, ok, mask, dst);
-    else tail_dispatch<T, NB, n + 1>(nn, x, y, t, ok, mask, dst);
-  }
-}
 
 template <typename T, int NB>
 __global__ void __launch_bounds__(kThreads)
@@ -432,10 +317,10 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
               const int64_t* __restrict__ OFF, int64_t N, T* __restrict__ out,
               int64_t* __restrict__ dom) {
   using A = Ar<T>;
-  constexpr int MQ = MaxShape<T>::Q(), ML = MaxShape<T>::L();
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   RaggedSmem<T, NB>& S = *reinterpret_cast<RaggedSmem<T, NB>*>(smem_raw);
   stage_table(S.st);
+  if (threadIdx.x == 0) { S.nQ = 0; S.nE = 0; }
   const int tid = threadIdx.x, lane = tid & 31;
   const int64_t ntiles = (N + kThreads - 1) / kThreads;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -445,107 +330,76 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
     const int64_t last = (i0 + kThreads < N) ? i0 + kThreads : N;
     const int64_t base = __ldg(OFF + i0);
     const int64_t cnt = __ldg(OFF + last) - base;
-    T x = in ? ldg_nc(X + i) : T(0);
+    const T x = in ? ldg_nc(X + i) : T(0);
     const int n = in ? (int)NM[i] : 0;
-    const int64_t off = in ? __ldg(OFF + i) - base : 0;
+    const int off = in ? (int)(__ldg(OFF + i) - base) : 0;
     const bool xok = valid_x(x);
     if (in && !(xok && n <= NB)) flag_domain(dom, i);
-    if (tid < NB + 2) S.hist[tid] = 0;
-    if (tid == 0) { S.nE = 0; S.nQ = 0; }
-    __syncthreads();   // previous tile fully stored; table staged (first pass)
+    // (1) previous tile fully stored and counters reset; table staged
     if (__syncthreads_or(in && n > NB)) {
-      // invalid order somewhere in the tile: direct writes, NaN for the bad ones
-      if (in) {
-        T* dst = out + base + off;
-        if (n > NB || !xok) {
-          for (int m = 0; m <= n; ++m) dst[m] = A::nan();
-        } else {
-          T Fv[NB + 1], t;
-          eval_point_rt<T, NB, MQ, ML>(x, true, n, S.st, Fv, t);
-          for (int m = 0; m <= n; ++m) dst[m] = Fv[m];
-        }
-      } else {
-        T Fv[NB + 1], t;
-        eval_point_rt<T, NB, MQ, ML>(T(0), true, 0, S.st, Fv, t);   // keep warps converged
+      // an order above the table in this tile: direct writes, NaN for bad ones
+      if (in && n > NB) {
+        for (int m = 0; m <= n; ++m) out[base + off + m] = A::nan();
       }
+      const bool okl = in && xok && n <= NB;
+      T* dst = out + base + off;
+      eval_point_rt<T, NB>(x, okl, okl ? n : 0, S.st, [&](int m, T v) {
+        if (in && n <= NB) dst[m] = v;
+      });
+      __syncthreads();
       continue;
     }
     const bool ok = in && xok;
     const T xs = ok ? x : T(0);
-    const bool needE = ok && xs <= A::XEXP;
     const bool needQ = ok && xs < S.st.row[n].z;
-    // stage + compaction (warp-aggregated atomics)
+    const bool needE = ok && !needQ && xs <= A::XEXP;
     S.sx[tid] = xs;
     S.sy[tid] = xs;
     S.stt[tid] = T(0);
-    S.sn[tid] = (unsigned char)n;
-    S.sok[tid] = ok;
-    S.soff[tid] = (int)off;
     {
-      unsigned bE = __ballot_sync(0xffffffffu, needE), bQ = __ballot_sync(0xffffffffu, needQ);
-      int baseE = 0, baseQ = 0;
+      const unsigned bQ = __ballot_sync(kFull, needQ), bE = __ballot_sync(kFull, needE);
+      int bq = 0, be = 0;
       if (lane == 0) {
-        baseE = atomicAdd(&S.nE, __popc(bE));
-        baseQ = atomicAdd(&S.nQ, __popc(bQ));
+        if (bQ) bq = atomicAdd(&S.nQ, __popc(bQ));
+        if (bE) be = atomicAdd(&S.nE, __popc(bE));
       }
-      baseE = __shfl_sync(0xffffffffu, baseE, 0);
-      baseQ = __shfl_sync(0xffffffffu, baseQ, 0);
-      unsigned lt = (1u << lane) - 1u;
-      if (needE) S.listE[baseE + __popc(bE & lt)] = (short)tid;
-      if (needQ) S.listQ[baseQ + __popc(bQ & lt)] = (short)tid;
+      bq = __shfl_sync(kFull, bq, 0);
+      be = __shfl_sync(kFull, be, 0);
+      const unsigned lt = (1u << lane) - 1u;
+      if (needQ) S.listQ[bq + __popc(bQ & lt)] = (short)(tid | (n << 9));
+      if (needE) S.listE[be + __popc(bE & lt)] = (short)tid;
     }
-    int rank_in_bin = in ? atomicAdd(&S.hist[n], 1) : 0;
-    __syncthreads();
-    // phase A1: e^{-x} on the compacted list
-    for (int k = tid; k < S.nE; k += kThreads) {
-      int e = S.listE[k];
-      S.stt[e] = exp_neg_clamped(S.sx[e]);
-    }
-    if (tid == 0) {   // exclusive scan of the order histogram
-      int acc = 0;
-      for (int b = 0; b <= NB; ++b) {
-        int h = S.hist[b];
-        S.hist[b] = acc;
-        acc += h;
+    __syncthreads();                                   // (2)
+    // phase A: e^{-x} for every listed element, y for those below the cut-off
+    {
+      const int nQ = S.nQ, tot = nQ + S.nE;
+      for (int k = tid; k < tot; k += kThreads) {
+        if (k < nQ) {
+          const int code = S.listQ[k];
+          const int e = code & 511, ne = code >> 9;
+          const T xe = S.sx[e];
+          const T te = exp_neg_clamped(xe);
+          S.stt[e] = te;
+          S.sy[e] = y_below_rt(xe, te, ne, S.st);
+        } else {
+          const int e = S.listE[k - nQ];
+          S.stt[e] = exp_neg_clamped(S.sx[e]);
+        }
       }
     }
-    __syncthreads();
-    // phase A2: y = x + Q~^{n+1/2} e^{-x} for elements below their cut-off
-    for (int k = tid; k < S.nQ; k += kThreads) {
-      int e = S.listQ[k];
-      int ne = S.sn[e];
-      const BoysRow<T>& R = S.st.row[ne];
-      T xe = S.sx[e];
-      T u = factored_rt<T, MQ, ML>(xe, R.uq, R.ul, S.st.shape[ne][0], S.st.shape[ne][1]);
-      T v = factored_rt<T, MQ, ML>(xe, R.vq, R.vl, S.st.shape[ne][2], S.st.shape[ne][3]);
-      T w = A::div(u, v);
-      T h = A::mul(R.q2, w);
-      h = A::fma(h, xe, R.q1);
-      T Q = A::fma(h, xe, R.q0);
-      T sq = A::sqrt(Q);
-      T s = ne == 0 ? sq : A::mul(powi_rt(Q, ne), sq);
-      S.sy[e] = A::fma(s, S.stt[e], xe);
+    __syncthreads();                                   // (3)
+    // phase B: per-lane tail, recursion bounded by the warp's largest order
+    {
+      const int wmax = __reduce_max_sync(kFull, (unsigned)(in ? n : 0));
+      T* dst = S.obuf + off;
+      tail_rt<T, NB>(xs, S.sy[tid], S.stt[tid], n, ok, wmax, S.st, [&](int m, T v) {
+        if (in) dst[m] = v;
+      });
     }
-    if (in) S.perm[S.hist[n] + rank_in_bin] = (short)tid;
-    __syncthreads();
-    // phase B: order-sorted tails
-    const int cntE = (int)(last - i0);
-    const bool has = tid < cntE;
-    const int e = has ? S.perm[tid] : 0;
-    const int ne = has ? S.sn[e] : 0;
-    unsigned todo = __ballot_sync(0xffffffffu, has);
-    while (todo) {
-      const int nl = __shfl_sync(0xffffffffu, ne, __ffs(todo) - 1);
-      const bool mine = has && ne == nl;
-      const unsigned mask = __ballot_sync(0xffffffffu, mine);
-      if (mine)
-        tail_dispatch<T, NB>(nl, S.sx[e], S.sy[e], S.stt[e], S.sok[e] != 0, mask,
-                             S.obuf + S.soff[e]);
-      todo &= ~mask;
-    }
-    __syncthreads();
-    T* dst = out + base;
-    for (int k = tid; k < (int)cnt; k += kThreads) __stcs(dst + k, S.obuf[k]);
+    if (tid == 0) { S.nQ = 0; S.nE = 0; }
+    __syncthreads();                                   // (4)
+    T* g = out + base;
+    for (int k = tid; k < (int)cnt; k += kThreads) __stcs(g + k, S.obuf[k]);
   }
 }
 
@@ -558,7 +412,6 @@ __global__ void __launch_bounds__(kThreads)
 split_kernel(const T* __restrict__ X, int64_t N, int nbar, T* __restrict__ out,
              int64_t* __restrict__ dom) {
   constexpr int W = n + 1;
-  constexpr int MQ = MaxShape<T>::Q(), ML = MaxShape<T>::L();
   __shared__ SmemTable<T> st;
   stage_table(st);
   __syncthreads();
@@ -570,18 +423,14 @@ split_kernel(const T* __restrict__ X, int64_t N, int nbar, T* __restrict__ out,
     bool ok = valid_x(x);
     if (in && !ok) flag_domain(dom, i);
     ok = ok || !in;
-    T Fv[W], Fl[W];
-    T t, tl;
-    eval_point<T, n>(in ? x : T(0), ok, Fv, t);
-    eval_point_rt<T, n, MQ, ML>(in ? x : T(0), ok, nbar, st, Fl, tl);
-    if (in) {
-#pragma unroll
-      for (int m = 0; m < W; ++m) {
-        T val = m <= nbar ? Fl[m] : Fv[m];
-        if (AOS) __stcs(out + i * W + m, val);
-        else __stcs(out + (int64_t)m * N + i, val);
-      }
-    }
+    T* o = AOS ? out + i * W : out + i;
+    const int64_t stride_m = AOS ? 1 : N;
+    eval_point_stream<T, n>(x, ok, [&](int m, T v) {
+      if (in && m > nbar) __stcs(o + m * stride_m, v);
+    });
+    eval_point_rt<T, n>(x, ok, nbar, st, [&](int m, T v) {
+      if (in && m <= nbar) __stcs(o + m * stride_m, v);
+    });
   }
 }
 
@@ -660,43 +509,38 @@ static boys_status cuda_status(cudaError_t e) {
   return BOYS_E_CUDA;
 }
 
-// Persistent grid (SMs x resident blocks) for large batches; for small ones
-// (<= 4 waves) one block per tile so the block scheduler balances the tail.
+// Persistent grid: SMs x resident blocks (measured better than one block per
+// tile even for the 2^20-point config: block launch overhead dominates there).
 template <typename K>
 static int blocks_for(K kernel, size_t smem, int64_t ntiles) {
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, smem);
   if (occ < 1) occ = 1;
   int64_t b = (int64_t)sm_count() * occ;
-  if (ntiles <= 4 * b) b = ntiles;
+  if (ntiles < b) b = ntiles;
   return (int)(b < 1 ? 1 : b);
 }
 
-// Tuning knobs (read once; defaults are the measured best on B200):
-//   BOYS_AOS_NBUF    staging depth (1 or 2)
-//   BOYS_DENSE_FLAGS bit0 prefetch next tile's x, bit1 per-warp bulk stores
-//   BOYS_RAGGED_V    ragged kernel variant (1 = predicated, 2 = compacted/sorted)
+// Tuning knobs (read once; defaults = measured best on B200):
+//   BOYS_AOS_NBUF  AoS staging depth per block (1 or 2)
+//   BOYS_AOS_MINB  AoS resident-block target handed to __launch_bounds__ (4 or 6)
 static int env_int(const char* name, int dflt) {
   const char* e = getenv(name);
   return e ? atoi(e) : dflt;
 }
 static int aos_nbuf() {
-  static int v = env_int("BOYS_AOS_NBUF", 2) == 1 ? 1 : 2;
+  static int v = env_int("BOYS_AOS_NBUF", 1) == 2 ? 2 : 1;
   return v;
 }
-static int dense_flags() {
-  static int v = env_int("BOYS_DENSE_FLAGS", 0);
-  return v;
-}
-static int ragged_variant() {
-  static int v = env_int("BOYS_RAGGED_V", 2);
+static int aos_minb() {
+  static int v = env_int("BOYS_AOS_MINB", 4) == 6 ? 6 : 4;
   return v;
 }
 
-template <typename T, int n, bool AOS, int NBUF>
+template <typename T, int n, bool AOS, int NBUF, int MINB>
 static boys_status launch_dense_k(const T* x, int64_t N, T* out, T* expx, int64_t* dom,
                                   int64_t base, cudaStream_t s) {
-  auto k = dense_kernel<T, n, AOS, NBUF>;
+  auto k = dense_kernel<T, n, AOS, NBUF, MINB>;
   size_t smem = AOS ? (size_t)NBUF * kThreads * (n + 1) * sizeof(T) : 0;
   static bool attr = false;   // per instantiation
   if (!attr) {
@@ -706,8 +550,7 @@ static boys_status launch_dense_k(const T* x, int64_t N, T* out, T* expx, int64_
   }
   int64_t ntiles = (N + kThreads - 1) / kThreads;
   bool bulk_ok = (reinterpret_cast<uintptr_t>(out) % 16) == 0;
-  k<<<blocks_for(k, smem, ntiles), kThreads, smem, s>>>(x, N, out, expx, dom, base, bulk_ok,
-                                                        dense_flags());
+  k<<<blocks_for(k, smem, ntiles), kThreads, smem, s>>>(x, N, out, expx, dom, base, bulk_ok);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cuda_status(cudaGetLastError());
 }
@@ -715,8 +558,13 @@ static boys_status launch_dense_k(const T* x, int64_t N, T* out, T* expx, int64_
 template <typename T, int n, bool AOS>
 static boys_status launch_dense_t(const T* x, int64_t N, T* out, T* expx, int64_t* dom,
                                   int64_t base, cudaStream_t s) {
-  if (AOS && aos_nbuf() == 1) return launch_dense_k<T, n, AOS, 1>(x, N, out, expx, dom, base, s);
-  return launch_dense_k<T, n, AOS, 2>(x, N, out, expx, dom, base, s);
+  if constexpr (!AOS) {
+    return launch_dense_k<T, n, false, 1, (n <= 1 ? 8 : 4)>(x, N, out, expx, dom, base, s);
+  } else {
+    if (aos_nbuf() == 2) return launch_dense_k<T, n, true, 2, 4>(x, N, out, expx, dom, base, s);
+    if (aos_minb() == 6) return launch_dense_k<T, n, true, 1, 6>(x, N, out, expx, dom, base, s);
+    return launch_dense_k<T, n, true, 1, 4>(x, N, out, expx, dom, base, s);
+  }
 }
 
 template <typename T, int n>
@@ -773,21 +621,16 @@ template <typename T>
 static boys_status launch_ragged(const void* x, const uint8_t* nm, const int64_t* off, int64_t N,
                                  void* out, int64_t* dom, cudaStream_t s) {
   constexpr int NB = Tab<T>::MAX_ORDER;
-  int64_t ntiles = (N + kThreads - 1) / kThreads;
-  if (ragged_variant() == 1) {
-    auto k = ragged_v1_kernel<T, NB>;
-    k<<<blocks_for(k, 0, ntiles), kThreads, 0, s>>>((const T*)x, nm, off, N, (T*)out, dom);
-  } else {
-    auto k = ragged_kernel<T, NB>;
-    const size_t smem = sizeof(RaggedSmem<T, NB>);
-    static bool attr = false;
-    if (!attr) {
-      cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return cuda_status(e);
-      attr = true;
-    }
-    k<<<blocks_for(k, smem, ntiles), kThreads, smem, s>>>((const T*)x, nm, off, N, (T*)out, dom);
+  auto k = ragged_kernel<T, NB>;
+  const size_t smem = sizeof(RaggedSmem<T, NB>);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return cuda_status(e);
+    attr = true;
   }
+  int64_t ntiles = (N + kThreads - 1) / kThreads;
+  k<<<blocks_for(k, smem, ntiles), kThreads, smem, s>>>((const T*)x, nm, off, N, (T*)out, dom);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cuda_status(cudaGetLastError());
 }
