@@ -246,7 +246,10 @@ __device__ __forceinline__ T powi_rt_bounded(T b, int n, int bits) {
 }
 
 // Tail for a run-time order n (per lane): F_n from y, then the recursion and
-// the upward ladder, handed to put(m, v).  `wmax` = warp-uniform max order.
+// the upward ladder, handed to put(m, v, on): `on` says whether m <= n, i.e.
+// whether the value is one of this lane's outputs (callers store
+// unconditionally to a scratch slot otherwise, so the loop stays branch-free).
+// `wmax` = warp-uniform max order bounds the loops.
 template <typename T, int NB, typename Put>
 __device__ __forceinline__ void tail_rt(T x, T y, T t, int n, bool ok, int wmax,
                                         const SmemTable<T>& st, Put&& put) {
@@ -257,26 +260,27 @@ __device__ __forceinline__ void tail_rt(T x, T y, T t, int n, bool ok, int wmax,
   T sr = A::sqrt(r);
   const T c = st.row[n].c;
   T cur = n == 0 ? A::mul(c, sr) : A::mul(A::mul(c, powi_rt_bounded(r, n, bits)), sr);
-  put(n, ok ? cur : bad);
+  put(n, ok ? cur : bad, true);
   T tx = A::add(x, x);
 #pragma unroll
   for (int m = NB - 1; m >= 0; --m) {
-    if (m >= wmax) continue;                       // warp-uniform
-    if (m < n) {
-      cur = A::mul(A::fma(tx, cur, t), rinv<T>(m));
-      put(m, ok ? cur : bad);
+    if (m < wmax) {                                // warp-uniform
+      T nx = A::mul(A::fma(tx, cur, t), rinv<T>(m));
+      const bool on = m < n;
+      cur = on ? nx : cur;
+      put(m, ok ? cur : bad, on);
     }
   }
   bool up = ok && x > st.row[n].x_up;
   if (__any_sync(kFull, up)) {
     T rx = A::rcp(x);
     T f = up_first(x);
-    if (up) put(0, f);
+    if (up) put(0, f, true);
 #pragma unroll
     for (int m = 0; m < NB; ++m) {
       if (m >= wmax) break;
       f = up_next(f, m, rx);
-      if (up && m + 1 <= n) put(m + 1, f);
+      if (up && m + 1 <= n) put(m + 1, f, true);
     }
   }
 }
@@ -296,7 +300,9 @@ __device__ __forceinline__ void eval_point_rt(T x_in, bool ok, int n, const Smem
     y = below ? yq : x;
   }
   int wmax = __reduce_max_sync(kFull, (unsigned)ns);
-  tail_rt<T, NB>(x, y, t, ns, ok, wmax, st, put);
+  tail_rt<T, NB>(x, y, t, ns, ok, wmax, st, [&](int m, T v, bool on) {
+    if (on) put(m, v);
+  });
 }
 
 // ---------------------------------------------------------------------------
@@ -306,8 +312,12 @@ template <typename T, int NB>
 struct RaggedSmem {
   SmemTable<T> st;
   T obuf[kThreads * (NB + 1)];
+  T scratch[kThreads];             // sink for the branch-free tail's off-range values
   T sx[kThreads], sy[kThreads], stt[kThreads];
-  short listQ[kThreads], listE[kThreads];
+  int soff[kThreads];
+  short listQ[kThreads], listE[kThreads], perm[kThreads];
+  unsigned char sn[kThreads], sok[kThreads];
+  int hist[NB + 2];
   int nQ, nE;
 };
 
@@ -321,6 +331,7 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
   RaggedSmem<T, NB>& S = *reinterpret_cast<RaggedSmem<T, NB>*>(smem_raw);
   stage_table(S.st);
   if (threadIdx.x == 0) { S.nQ = 0; S.nE = 0; }
+  if (threadIdx.x <= NB) S.hist[threadIdx.x] = 0;
   const int tid = threadIdx.x, lane = tid & 31;
   const int64_t ntiles = (N + kThreads - 1) / kThreads;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -356,6 +367,19 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
     S.sx[tid] = xs;
     S.sy[tid] = xs;
     S.stt[tid] = T(0);
+    S.soff[tid] = off;
+    S.sn[tid] = (unsigned char)n;
+    S.sok[tid] = ok;
+    // rank of this element within its order bucket (warp-aggregated)
+    int rank_in_bin = 0;
+    {
+      const unsigned peers = __match_any_sync(kFull, in ? n : -1);
+      const int leader = __ffs(peers) - 1;
+      int b0 = 0;
+      if (in && lane == leader) b0 = atomicAdd(&S.hist[n], __popc(peers));
+      b0 = __shfl_sync(kFull, b0, leader);
+      rank_in_bin = b0 + __popc(peers & ((1u << lane) - 1u));
+    }
     {
       const unsigned bQ = __ballot_sync(kFull, needQ), bE = __ballot_sync(kFull, needE);
       int bq = 0, be = 0;
@@ -370,6 +394,16 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
       if (needE) S.listE[be + __popc(bE & lt)] = (short)tid;
     }
     __syncthreads();                                   // (2)
+    if (tid < 32) {                                    // exclusive scan of the order histogram
+      const int h = tid <= NB ? S.hist[tid] : 0;
+      int v = h;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int o = __shfl_up_sync(kFull, v, d);
+        if (tid >= d) v += o;
+      }
+      if (tid <= NB) S.hist[tid] = v - h;
+    }
     // phase A: e^{-x} for every listed element, y for those below the cut-off
     {
       const int nQ = S.nQ, tot = nQ + S.nE;
@@ -387,16 +421,24 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
         }
       }
     }
-    __syncthreads();                                   // (3)
-    // phase B: per-lane tail, recursion bounded by the warp's largest order
+    __syncthreads();                                   // (3) scan + phase A done
+    if (in) S.perm[S.hist[n] + rank_in_bin] = (short)tid;
+    __syncthreads();                                   // (3b)
+    // phase B: lanes take elements in order-sorted sequence (warps hold nearly
+    // uniform orders); per-lane tail bounded by the warp's largest order
     {
-      const int wmax = __reduce_max_sync(kFull, (unsigned)(in ? n : 0));
-      T* dst = S.obuf + off;
-      tail_rt<T, NB>(xs, S.sy[tid], S.stt[tid], n, ok, wmax, S.st, [&](int m, T v) {
-        if (in) dst[m] = v;
-      });
+      const int cntE = (int)(last - i0);
+      const bool has = tid < cntE;
+      const int e = has ? S.perm[tid] : 0;
+      const int ne = has ? S.sn[e] : 0;
+      const int wmax = __reduce_max_sync(kFull, (unsigned)ne);
+      T* dst = S.obuf + (has ? S.soff[e] : 0);
+      T* sink = S.scratch + tid;
+      tail_rt<T, NB>(S.sx[e], S.sy[e], S.stt[e], ne, has && S.sok[e], wmax, S.st,
+                     [&](int m, T v, bool on) { *((has && on) ? dst + m : sink) = v; });
     }
     if (tid == 0) { S.nQ = 0; S.nE = 0; }
+    if (tid <= NB) S.hist[tid] = 0;
     __syncthreads();                                   // (4)
     T* g = out + base;
     for (int k = tid; k < (int)cnt; k += kThreads) __stcs(g + k, S.obuf[k]);
