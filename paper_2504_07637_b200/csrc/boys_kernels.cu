@@ -307,19 +307,53 @@ __device__ __forceinline__ void eval_point_rt(T x_in, bool ok, int n, const Smem
 
 // ---------------------------------------------------------------------------
 // ragged kernel: element i, order n_i, values at out[offsets[i] + m]
+//
+// Warp-autonomous (no block barriers): each warp walks 32-element chunks.
+//   * every lane: e^{-x}; elements past their cut-off (x >= z_{n_i}, ~95% of
+//     ERI-like batches) run the cheap run-time-order tail at once into the
+//     warp's staging slot; the chunk's contiguous output range then leaves
+//     with coalesced streaming stores (skipping deferred elements).
+//   * elements below their cut-off are deferred to a warp-private queue and
+//     evaluated 32 at a time with every lane busy (Q~ is the expensive part),
+//     each lane writing its element's n+1 values directly.
+// Values are bit-identical to boys_eval_dense at each element's order.
 // ---------------------------------------------------------------------------
+template <typename T, int NB>
+struct RaggedWarp {
+  T stage[32 * (NB + 1)];
+  T qx[64], qt[64];
+  int64_t qoff[64];
+  unsigned char qn[64];
+  T scratch[32];
+};
+
 template <typename T, int NB>
 struct RaggedSmem {
   SmemTable<T> st;
-  T obuf[kThreads * (NB + 1)];
-  T scratch[kThreads];             // sink for the branch-free tail's off-range values
-  T sx[kThreads], sy[kThreads], stt[kThreads];
-  int soff[kThreads];
-  short listQ[kThreads], listE[kThreads], perm[kThreads];
-  unsigned char sn[kThreads], sok[kThreads];
-  int hist[NB + 2];
-  int nQ, nE;
+  RaggedWarp<T, NB> w[kThreads / 32];
 };
+
+// Evaluate up to 32 queued below-cut-off elements (one per lane), writing
+// straight to global memory.
+template <typename T, int NB>
+__device__ __forceinline__ void ragged_drain(RaggedWarp<T, NB>& W, const SmemTable<T>& st,
+                                             int& qn, int lane, T* __restrict__ out) {
+  const int take = qn < 32 ? qn : 32;
+  const bool has = lane < take;
+  const int slot = qn - take + lane;            // LIFO: drain the newest `take` entries
+  const T x = has ? W.qx[slot] : T(0);
+  const T t = has ? W.qt[slot] : T(0);
+  const int n = has ? (int)W.qn[slot] : 0;
+  const int64_t off = has ? W.qoff[slot] : 0;
+  __syncwarp();
+  const T y = has ? y_below_rt(x, t, n, st) : x;
+  const int wmax = __reduce_max_sync(kFull, (unsigned)n);
+  T* dst = out + off;
+  T* sink = W.scratch + lane;
+  tail_rt<T, NB>(x, y, t, n, has, wmax, st,
+                 [&](int m, T v, bool on) { *((has && on) ? dst + m : sink) = v; });
+  qn -= take;
+}
 
 template <typename T, int NB>
 __global__ void __launch_bounds__(kThreads)
@@ -330,119 +364,88 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
   extern __shared__ __align__(128) unsigned char smem_raw[];
   RaggedSmem<T, NB>& S = *reinterpret_cast<RaggedSmem<T, NB>*>(smem_raw);
   stage_table(S.st);
-  if (threadIdx.x == 0) { S.nQ = 0; S.nE = 0; }
-  if (threadIdx.x <= NB) S.hist[threadIdx.x] = 0;
-  const int tid = threadIdx.x, lane = tid & 31;
-  const int64_t ntiles = (N + kThreads - 1) / kThreads;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t i0 = tile * kThreads;
-    const int64_t i = i0 + tid;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  RaggedWarp<T, NB>& W = S.w[wid];
+  const int64_t nchunks = (N + 31) / 32;
+  const int64_t wstride = (int64_t)gridDim.x * (kThreads / 32);
+  int qn = 0;                                    // warp-uniform queue length
+  for (int64_t c = (int64_t)blockIdx.x * (kThreads / 32) + wid; c < nchunks; c += wstride) {
+    const int64_t i0 = c * 32;
+    const int64_t i = i0 + lane;
     const bool in = i < N;
-    const int64_t last = (i0 + kThreads < N) ? i0 + kThreads : N;
+    const int64_t last = (i0 + 32 < N) ? i0 + 32 : N;
     const int64_t base = __ldg(OFF + i0);
     const int64_t cnt = __ldg(OFF + last) - base;
     const T x = in ? ldg_nc(X + i) : T(0);
     const int n = in ? (int)NM[i] : 0;
-    const int off = in ? (int)(__ldg(OFF + i) - base) : 0;
+    const int64_t goff = in ? __ldg(OFF + i) : 0;
     const bool xok = valid_x(x);
     if (in && !(xok && n <= NB)) flag_domain(dom, i);
-    // (1) previous tile fully stored and counters reset; table staged
-    if (__syncthreads_or(in && n > NB)) {
-      // an order above the table in this tile: direct writes, NaN for bad ones
+    if (__any_sync(kFull, in && n > NB)) {
+      // an order above the table: every lane writes its own values directly
       if (in && n > NB) {
-        for (int m = 0; m <= n; ++m) out[base + off + m] = A::nan();
+        for (int m = 0; m <= n; ++m) out[goff + m] = A::nan();
       }
       const bool okl = in && xok && n <= NB;
-      T* dst = out + base + off;
+      T* dst = out + goff;
       eval_point_rt<T, NB>(x, okl, okl ? n : 0, S.st, [&](int m, T v) {
         if (in && n <= NB) dst[m] = v;
       });
-      __syncthreads();
       continue;
     }
     const bool ok = in && xok;
     const T xs = ok ? x : T(0);
-    const bool needQ = ok && xs < S.st.row[n].z;
-    const bool needE = ok && !needQ && xs <= A::XEXP;
-    S.sx[tid] = xs;
-    S.sy[tid] = xs;
-    S.stt[tid] = T(0);
-    S.soff[tid] = off;
-    S.sn[tid] = (unsigned char)n;
-    S.sok[tid] = ok;
-    // rank of this element within its order bucket (warp-aggregated)
-    int rank_in_bin = 0;
-    {
-      const unsigned peers = __match_any_sync(kFull, in ? n : -1);
-      const int leader = __ffs(peers) - 1;
-      int b0 = 0;
-      if (in && lane == leader) b0 = atomicAdd(&S.hist[n], __popc(peers));
-      b0 = __shfl_sync(kFull, b0, leader);
-      rank_in_bin = b0 + __popc(peers & ((1u << lane) - 1u));
-    }
-    {
-      const unsigned bQ = __ballot_sync(kFull, needQ), bE = __ballot_sync(kFull, needE);
-      int bq = 0, be = 0;
-      if (lane == 0) {
-        if (bQ) bq = atomicAdd(&S.nQ, __popc(bQ));
-        if (bE) be = atomicAdd(&S.nE, __popc(bE));
+    const T t = exp_neg_clamped(xs);
+    const bool defer = ok && xs < S.st.row[n].z;
+    const unsigned dmask = __ballot_sync(kFull, defer);
+    if (dmask) {                                   // enqueue (qn stays warp-uniform)
+      if (defer) {
+        const int slot = qn + __popc(dmask & ((1u << lane) - 1u));
+        W.qx[slot] = xs;
+        W.qt[slot] = t;
+        W.qn[slot] = (unsigned char)n;
+        W.qoff[slot] = goff;
       }
-      bq = __shfl_sync(kFull, bq, 0);
-      be = __shfl_sync(kFull, be, 0);
-      const unsigned lt = (1u << lane) - 1u;
-      if (needQ) S.listQ[bq + __popc(bQ & lt)] = (short)(tid | (n << 9));
-      if (needE) S.listE[be + __popc(bE & lt)] = (short)tid;
+      qn += __popc(dmask);
+      __syncwarp();
     }
-    __syncthreads();                                   // (2)
-    if (tid < 32) {                                    // exclusive scan of the order histogram
-      const int h = tid <= NB ? S.hist[tid] : 0;
-      int v = h;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const int o = __shfl_up_sync(kFull, v, d);
-        if (tid >= d) v += o;
-      }
-      if (tid <= NB) S.hist[tid] = v - h;
-    }
-    // phase A: e^{-x} for every listed element, y for those below the cut-off
+    // immediate elements: tail into the staging slot
     {
-      const int nQ = S.nQ, tot = nQ + S.nE;
-      for (int k = tid; k < tot; k += kThreads) {
-        if (k < nQ) {
-          const int code = S.listQ[k];
-          const int e = code & 511, ne = code >> 9;
-          const T xe = S.sx[e];
-          const T te = exp_neg_clamped(xe);
-          S.stt[e] = te;
-          S.sy[e] = y_below_rt(xe, te, ne, S.st);
-        } else {
-          const int e = S.listE[k - nQ];
-          S.stt[e] = exp_neg_clamped(S.sx[e]);
+      const int loc = (int)(goff - base);
+      const int wmax = __reduce_max_sync(kFull, (unsigned)((in && !defer) ? n : 0));
+      T* dst = W.stage + loc;
+      T* sink = W.scratch + lane;
+      const bool wr = in && !defer;
+      tail_rt<T, NB>(xs, xs, t, n, ok, wmax, S.st,
+                     [&](int m, T v, bool on) { *((wr && on) ? dst + m : sink) = v; });
+    }
+    __syncwarp();
+    // coalesced copy of the chunk's range, skipping deferred elements' values
+    {
+      const int ncnt = (int)cnt;
+      T* g = out + base;
+      if (!dmask) {
+        for (int k = lane; k < ncnt; k += 32) __stcs(g + k, W.stage[k]);
+      } else {
+        const int loc = (int)(goff - base);
+        for (int k = lane; k < ncnt; k += 32) {
+          bool skip = false;
+          unsigned mm = dmask;
+          while (mm) {                               // usually one or two entries
+            const int j = __ffs(mm) - 1;
+            mm &= mm - 1;
+            const int s0 = __shfl_sync(kFull, loc, j), s1 = s0 + __shfl_sync(kFull, n, j);
+            skip = skip || (k >= s0 && k <= s1);
+          }
+          if (!skip) __stcs(g + k, W.stage[k]);
         }
       }
     }
-    __syncthreads();                                   // (3) scan + phase A done
-    if (in) S.perm[S.hist[n] + rank_in_bin] = (short)tid;
-    __syncthreads();                                   // (3b)
-    // phase B: lanes take elements in order-sorted sequence (warps hold nearly
-    // uniform orders); per-lane tail bounded by the warp's largest order
-    {
-      const int cntE = (int)(last - i0);
-      const bool has = tid < cntE;
-      const int e = has ? S.perm[tid] : 0;
-      const int ne = has ? S.sn[e] : 0;
-      const int wmax = __reduce_max_sync(kFull, (unsigned)ne);
-      T* dst = S.obuf + (has ? S.soff[e] : 0);
-      T* sink = S.scratch + tid;
-      tail_rt<T, NB>(S.sx[e], S.sy[e], S.stt[e], ne, has && S.sok[e], wmax, S.st,
-                     [&](int m, T v, bool on) { *((has && on) ? dst + m : sink) = v; });
-    }
-    if (tid == 0) { S.nQ = 0; S.nE = 0; }
-    if (tid <= NB) S.hist[tid] = 0;
-    __syncthreads();                                   // (4)
-    T* g = out + base;
-    for (int k = tid; k < (int)cnt; k += kThreads) __stcs(g + k, S.obuf[k]);
+    __syncwarp();
+    if (qn >= 32) ragged_drain<T, NB>(W, S.st, qn, lane, out);
   }
+  while (qn > 0) ragged_drain<T, NB>(W, S.st, qn, lane, out);
 }
 
 // ---------------------------------------------------------------------------
@@ -571,7 +574,7 @@ static int env_int(const char* name, int dflt) {
   return e ? atoi(e) : dflt;
 }
 static int aos_nbuf() {
-  static int v = env_int("BOYS_AOS_NBUF", 1) == 2 ? 2 : 1;
+  static int v = env_int("BOYS_AOS_NBUF", 2) == 1 ? 1 : 2;
   return v;
 }
 static int aos_minb() {
