@@ -429,7 +429,8 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
         for (int k = lane; k < ncnt; k += 32) __stcs(g + k, W.stage[k]);
       } else {
         const int loc = (int)(goff - base);
-        for (int k = lane; k < ncnt; k += 32) {
+        for (int k0 = 0; k0 < ncnt; k0 += 32) {     // warp-uniform trip count
+          const int k = k0 + lane;
           bool skip = false;
           unsigned mm = dmask;
           while (mm) {                               // usually one or two entries
@@ -438,7 +439,7 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
             const int s0 = __shfl_sync(kFull, loc, j), s1 = s0 + __shfl_sync(kFull, n, j);
             skip = skip || (k >= s0 && k <= s1);
           }
-          if (!skip) __stcs(g + k, W.stage[k]);
+          if (k < ncnt && !skip) __stcs(g + k, W.stage[k]);
         }
       }
     }

@@ -1,0 +1,16 @@
+mkdir -p gpurun_out
+timeout 300 python -m pytest tests/test_gpu_parity.py tests/test_gpu_accuracy.py -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1
+rc=$?; echo "pytest rc=$rc" >> gpurun_out/pytest_gpu.log; tail -n 4 gpurun_out/pytest_gpu.log
+if [ $rc -ne 0 ]; then exit 1; fi
+out=gpurun_out/ab.txt; : > $out
+run() {
+  local cfg=$1; shift
+  local line
+  line=$(env "$@" timeout 120 python bench.py --config $cfg --steps 200 --warmup 5 --no-extras --e2e-steps 0 --cpu-seconds 0 2>&1 | grep '^{')
+  echo "$cfg $* :: $(echo "$line" | python3 -c 'import json,sys; d=json.loads(sys.stdin.read()); r=d["roofline"]; print("frac=%.4f launch_ms=%.4f val=%.4g clk=%s" % (r["frac"], r["launch_ms"], d["value"], d["clocks"]["sm_mhz"]))')" >> $out
+}
+run cfg4 X=1 && run cfg4f32 X=1 && run cfg4 X=2 && run cfg4f32 X=2
+cat $out
+timeout 120 python tools/prof_kernels.py --configs cfg4,cfg4f32 --launches 2 > gpurun_out/prof_plain.log 2>&1 && \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"ragged_kernel" -s 1 -c 2 \
+    -o gpurun_out/prof_v5 python tools/prof_kernels.py --configs cfg4,cfg4f32 --launches 2 > gpurun_out/ncu_v5.log 2>&1
