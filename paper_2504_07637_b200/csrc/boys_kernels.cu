@@ -355,6 +355,18 @@ __device__ __forceinline__ void ragged_drain(RaggedWarp<T, NB>& W, const SmemTab
   qn -= take;
 }
 
+// Staging sentinel for deferred elements' slots: a NaN payload the arithmetic
+// never produces (IEEE ops return the canonical quiet NaN).
+template <typename T> struct Sentinel;
+template <> struct Sentinel<double> {
+  static __device__ __forceinline__ double value() { return __longlong_as_double(0x7ff4c0de5e47e1e1LL); }
+  static __device__ __forceinline__ bool is(double v) { return __double_as_longlong(v) == 0x7ff4c0de5e47e1e1LL; }
+};
+template <> struct Sentinel<float> {
+  static __device__ __forceinline__ float value() { return __int_as_float(0x7fa0c0de); }
+  static __device__ __forceinline__ bool is(float v) { return __float_as_int(v) == 0x7fa0c0de; }
+};
+
 template <typename T, int NB>
 __global__ void __launch_bounds__(kThreads)
 ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
@@ -370,16 +382,31 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
   const int64_t nchunks = (N + 31) / 32;
   const int64_t wstride = (int64_t)gridDim.x * (kThreads / 32);
   int qn = 0;                                    // warp-uniform queue length
-  for (int64_t c = (int64_t)blockIdx.x * (kThreads / 32) + wid; c < nchunks; c += wstride) {
+  int64_t c = (int64_t)blockIdx.x * (kThreads / 32) + wid;
+  // software pipeline: inputs of chunk c are loaded one iteration ahead
+  T px = T(0);
+  int pn = 0;
+  int64_t poff = 0, pbase = 0, plast_off = 0;
+  auto load = [&](int64_t cc) {
+    const int64_t j0 = cc * 32, j = j0 + lane;
+    const bool jin = cc < nchunks && j < N;
+    px = jin ? ldg_nc(X + j) : T(0);
+    pn = jin ? (int)NM[j] : 0;
+    poff = jin ? __ldg(OFF + j) : 0;
+    if (cc < nchunks) {
+      pbase = __ldg(OFF + j0);
+      plast_off = __ldg(OFF + ((j0 + 32 < N) ? j0 + 32 : N));
+    }
+  };
+  load(c);
+  for (; c < nchunks; c += wstride) {
     const int64_t i0 = c * 32;
     const int64_t i = i0 + lane;
     const bool in = i < N;
-    const int64_t last = (i0 + 32 < N) ? i0 + 32 : N;
-    const int64_t base = __ldg(OFF + i0);
-    const int64_t cnt = __ldg(OFF + last) - base;
-    const T x = in ? ldg_nc(X + i) : T(0);
-    const int n = in ? (int)NM[i] : 0;
-    const int64_t goff = in ? __ldg(OFF + i) : 0;
+    const T x = px;
+    const int n = pn;
+    const int64_t goff = poff, base = pbase, cnt = plast_off - pbase;
+    load(c + wstride);
     const bool xok = valid_x(x);
     if (in && !(xok && n <= NB)) flag_domain(dom, i);
     if (__any_sync(kFull, in && n > NB)) {
@@ -395,51 +422,70 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
       continue;
     }
     const bool ok = in && xok;
-    const T xs = ok ? x : T(0);
-    const T t = exp_neg_clamped(xs);
-    const bool defer = ok && xs < S.st.row[n].z;
+    const T xs = ok ? x : A::nan();                // NaN propagates through the tail
+    const T xe = ok ? x : T(0);
+    const T t = exp_neg_clamped(xe);
+    const bool defer = ok && xe < S.st.row[n].z;
     const unsigned dmask = __ballot_sync(kFull, defer);
+    const int loc = (int)(goff - base);
+    T* dst = W.stage + loc;
     if (dmask) {                                   // enqueue (qn stays warp-uniform)
       if (defer) {
         const int slot = qn + __popc(dmask & ((1u << lane) - 1u));
-        W.qx[slot] = xs;
+        W.qx[slot] = xe;
         W.qt[slot] = t;
         W.qn[slot] = (unsigned char)n;
         W.qoff[slot] = goff;
+        for (int m = 0; m <= n; ++m) dst[m] = Sentinel<T>::value();
       }
       qn += __popc(dmask);
-      __syncwarp();
     }
-    // immediate elements: tail into the staging slot
+    // immediate elements (past the cut-off): y = x.  Same operation sequence as
+    // seed<T, n> + the recursion + the upward ladder.
     {
-      const int loc = (int)(goff - base);
-      const int wmax = __reduce_max_sync(kFull, (unsigned)((in && !defer) ? n : 0));
-      T* dst = W.stage + loc;
-      T* sink = W.scratch + lane;
       const bool wr = in && !defer;
-      tail_rt<T, NB>(xs, xs, t, n, ok, wmax, S.st,
-                     [&](int m, T v, bool on) { *((wr && on) ? dst + m : sink) = v; });
+      const int wmax = __reduce_max_sync(kFull, (unsigned)(wr ? n : 0));
+      const int bits = 32 - __clz(wmax | 1);
+      const T r = A::rcp(xs);
+      const T sr = A::sqrt(r);
+      const T cn = S.st.row[n].c;
+      T cur = n == 0 ? A::mul(cn, sr) : A::mul(A::mul(cn, powi_rt_bounded(r, n, bits)), sr);
+      if (wr) dst[n] = cur;
+      const T tx = A::add(xs, xs);
+#pragma unroll
+      for (int m = NB - 1; m >= 0; --m) {
+        if (m < wmax) {                            // warp-uniform
+          const T nx = A::mul(A::fma(tx, cur, t), rinv<T>(m));
+          const bool on = m < n;
+          cur = on ? nx : cur;
+          if (wr && on) dst[m] = cur;
+        }
+      }
+      const bool up = wr && ok && xs > S.st.row[n].x_up;
+      if (__any_sync(kFull, up)) {
+        const T rx = A::rcp(xs);
+        T f = up_first(xs);
+        if (up) dst[0] = f;
+#pragma unroll
+        for (int m = 0; m < NB; ++m) {
+          if (m >= wmax) break;
+          f = up_next(f, m, rx);
+          if (up && m + 1 <= n) dst[m + 1] = f;
+        }
+      }
     }
     __syncwarp();
-    // coalesced copy of the chunk's range, skipping deferred elements' values
+    // coalesced copy of the chunk's range; deferred elements' slots hold the
+    // sentinel and are skipped (their values are written by the drain)
     {
       const int ncnt = (int)cnt;
       T* g = out + base;
       if (!dmask) {
         for (int k = lane; k < ncnt; k += 32) __stcs(g + k, W.stage[k]);
       } else {
-        const int loc = (int)(goff - base);
-        for (int k0 = 0; k0 < ncnt; k0 += 32) {     // warp-uniform trip count
-          const int k = k0 + lane;
-          bool skip = false;
-          unsigned mm = dmask;
-          while (mm) {                               // usually one or two entries
-            const int j = __ffs(mm) - 1;
-            mm &= mm - 1;
-            const int s0 = __shfl_sync(kFull, loc, j), s1 = s0 + __shfl_sync(kFull, n, j);
-            skip = skip || (k >= s0 && k <= s1);
-          }
-          if (k < ncnt && !skip) __stcs(g + k, W.stage[k]);
+        for (int k = lane; k < ncnt; k += 32) {
+          const T v = W.stage[k];
+          if (!Sentinel<T>::is(v)) __stcs(g + k, v);
         }
       }
     }
