@@ -240,7 +240,7 @@ __device__ __forceinline__ T powi_rt_bounded(T b, int n, int bits) {
     T rr = have ? A::mul(r, p) : p;
     r = bit ? rr : r;
     have = have || bit;
-    if ((n >> (j + 1)) != 0) p = A::mul(p, p);
+    p = A::mul(p, p);      // unused past the top bit of n: no effect on r
   }
   return r;
 }
@@ -320,7 +320,7 @@ __device__ __forceinline__ void eval_point_rt(T x_in, bool ok, int n, const Smem
 // ---------------------------------------------------------------------------
 template <typename T, int NB>
 struct RaggedWarp {
-  T stage[32 * (NB + 1)];
+  alignas(16) T stage[32 * (NB + 1) + 16 / sizeof(T)];
   T qx[64], qt[64];
   int64_t qoff[64];
   unsigned char qn[64];
@@ -338,6 +338,10 @@ struct RaggedSmem {
 template <typename T, int NB>
 __device__ __forceinline__ void ragged_drain(RaggedWarp<T, NB>& W, const SmemTable<T>& st,
                                              int& qn, int lane, T* __restrict__ out) {
+  // queued elements' slots were written (with stale staging data) by earlier
+  // bulk stores of their chunks: those must be complete before we overwrite
+  if (lane == 0) bulk_wait_all();
+  __syncwarp();
   const int take = qn < 32 ? qn : 32;
   const bool has = lane < take;
   const int slot = qn - take + lane;            // LIFO: drain the newest `take` entries
@@ -427,7 +431,13 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
     const T t = exp_neg_clamped(xe);
     const bool defer = ok && xe < S.st.row[n].z;
     const unsigned dmask = __ballot_sync(kFull, defer);
-    const int loc = (int)(goff - base);
+    // staging position matches the global 16-byte phase of the chunk range
+    constexpr int Q = 16 / sizeof(T);
+    const int shift = (int)(base & (Q - 1));
+    const int loc = (int)(goff - base) + shift;
+    // the previous chunk's bulk store must have finished reading the slot
+    if (lane == 0) bulk_wait_read<0>();
+    __syncwarp();
     T* dst = W.stage + loc;
     if (dmask) {                                   // enqueue (qn stays warp-uniform)
       if (defer) {
@@ -436,7 +446,6 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
         W.qt[slot] = t;
         W.qn[slot] = (unsigned char)n;
         W.qoff[slot] = goff;
-        for (int m = 0; m <= n; ++m) dst[m] = Sentinel<T>::value();
       }
       qn += __popc(dmask);
     }
@@ -455,10 +464,10 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
 #pragma unroll
       for (int m = NB - 1; m >= 0; --m) {
         if (m < wmax) {                            // warp-uniform
-          const T nx = A::mul(A::fma(tx, cur, t), rinv<T>(m));
-          const bool on = m < n;
-          cur = on ? nx : cur;
-          if (wr && on) dst[m] = cur;
+          if (m < n) {                             // predicated, no select
+            cur = A::mul(A::fma(tx, cur, t), rinv<T>(m));
+            if (wr) dst[m] = cur;
+          }
         }
       }
       const bool up = wr && ok && xs > S.st.row[n].x_up;
@@ -475,24 +484,26 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
       }
     }
     __syncwarp();
-    // coalesced copy of the chunk's range; deferred elements' slots hold the
-    // sentinel and are skipped (their values are written by the drain)
+    // the chunk's output range [base, base + cnt): scalar head/tail to reach
+    // 16-byte alignment, one bulk async copy (TMA engine) for the body.
+    // Deferred elements' slots go out stale and are rewritten by the drain.
     {
       const int ncnt = (int)cnt;
-      T* g = out + base;
-      if (!dmask) {
-        for (int k = lane; k < ncnt; k += 32) __stcs(g + k, W.stage[k]);
-      } else {
-        for (int k = lane; k < ncnt; k += 32) {
-          const T v = W.stage[k];
-          if (!Sentinel<T>::is(v)) __stcs(g + k, v);
-        }
+      const int head = ((Q - shift) & (Q - 1)) < ncnt ? ((Q - shift) & (Q - 1)) : ncnt;
+      const int body = ((ncnt - head) / Q) * Q;
+      const int tail0 = head + body;
+      if (lane < head) __stcs(out + base + lane, W.stage[shift + lane]);
+      if (lane < ncnt - tail0) __stcs(out + base + tail0 + lane, W.stage[shift + tail0 + lane]);
+      if (body > 0) {
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) bulk_store(out + base + head, W.stage + shift + head, body * sizeof(T));
       }
     }
-    __syncwarp();
     if (qn >= 32) ragged_drain<T, NB>(W, S.st, qn, lane, out);
   }
   while (qn > 0) ragged_drain<T, NB>(W, S.st, qn, lane, out);
+  if (lane == 0) bulk_wait_all();
 }
 
 // ---------------------------------------------------------------------------
