@@ -54,27 +54,33 @@ UNIT = "values/s"
 # infrastructure
 # ----------------------------------------------------------------------------
 
+def _dist_on() -> bool:
+    import torch.distributed as dist
+    return dist.is_available() and dist.is_initialized()
+
+
 def dist_setup(gpus: int):
+    """One process per GPU.  Under torchrun (RANK set) the NCCL group is
+    created even at world size 1, so the barrier / max-over-ranks / gather
+    paths are the same code at every N."""
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if ws > 1:
+    torch.cuda.set_device(local)
+    if "RANK" in os.environ:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:
-        torch.cuda.set_device(0)
     return rank, ws, local
 
 
 def barrier(ws):
-    if ws > 1:
+    if _dist_on():
         import torch.distributed as dist
         dist.barrier()
 
 
 def max_over_ranks(v: float, ws: int) -> float:
-    if ws == 1:
+    if not _dist_on():
         return v
     import torch.distributed as dist
     t = torch.tensor([v], dtype=torch.float64, device="cuda")
@@ -83,7 +89,7 @@ def max_over_ranks(v: float, ws: int) -> float:
 
 
 def sum_over_ranks(v: float, ws: int) -> float:
-    if ws == 1:
+    if not _dist_on():
         return v
     import torch.distributed as dist
     t = torch.tensor([v], dtype=torch.float64, device="cuda")
@@ -190,10 +196,12 @@ class Dense:
         self.layout = cfg.layout
         total = n_points or cfg.N
         if cfg.name == "cfg5":          # strong scaling: shard 2^30 contiguously
-            nch = total // W.CHUNK
-            per = nch // ws
-            self.chunks = list(range(rank * per, (rank + 1) * per))
-            self.xs = [W.config_x("cfg5", n=W.CHUNK, chunk=c, device=dev) for c in self.chunks]
+            from paper_2504_07637_b200 import shard as S
+            plan = S.chunk_plan(total, rank, ws, W.CHUNK)
+            self.chunks = [cid for cid, _, _ in plan]
+            self.xs = [W.config_x("cfg5", n=W.CHUNK, chunk=cid, device=dev)[lo - cid * W.CHUNK:
+                                                                          hi - cid * W.CHUNK]
+                       for cid, lo, hi in plan]
             self.outs = [torch.empty(self._shape(W.CHUNK), dtype=torch.float64, device=dev)
                          for _ in range(2)]
             self.scaling = "strong"
@@ -214,6 +222,8 @@ class Dense:
         from paper_2504_07637_b200 import boys
         for k, x in enumerate(self.xs):
             out = self.outs[k % len(self.outs)]
+            if self.layout == "aos":
+                out = out[: x.numel()]          # contiguous prefix for a partial chunk
             yield lambda x=x, out=out: boys(self.n, x, layout=self.layout, out=out, check=False)
 
 
@@ -400,6 +410,25 @@ def e2e_dense(cfg_name, steps, dev):
                                     "(chunked H2D / kernel / D2H pipeline)"}
 
 
+def golden_check(cfg_name, rank, ws, dev):
+    """Max relative error vs refmath.boys_downward goldens (tests/golden,
+    double-double), gathered over ranks with all_gather (1 fp64 per rank)."""
+    import math
+    from paper_2504_07637_b200 import boys, shard as S, workloads as W
+    cfg = W.CONFIGS[cfg_name]
+    if cfg.layout == "ragged":
+        return None
+    d = np.load(ROOT / "tests" / "golden" / "configs.npz")
+    gx = torch.from_numpy(d[f"{cfg_name}_x"]).to(dev)
+    gF = torch.from_numpy(d[f"{cfg_name}_F"]).to(dev)
+    err = S.golden_error(cfg.n_max, gx, gF, rank, ws,
+                         lambda n, x: boys(n, x.contiguous(), layout="aos"))
+    per_rank, mx = S.gather_max(err)
+    return {"golden_points": int(gx.numel()), "max_rel_err": mx,
+            "bits": (-math.log2(mx) if mx > 0 else None), "per_rank": per_rank,
+            "reference": "refmath.boys_downward(n, x, Precision(96)), tests/golden/configs.npz"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -451,6 +480,13 @@ def main():
         "clocks": clocks,
         "gpu_launches": launches,
     }
+
+    # accuracy: each rank checks its slice of the reference-golden sample on
+    # the device; one fp64 per rank is gathered (the path's only collective)
+    try:
+        line["accuracy"] = golden_check(args.config, rank, ws, dev)
+    except Exception as ex:  # noqa: BLE001
+        line["accuracy"] = {"error": str(ex)[:200]}
 
     # end-to-end (host buffers through the C-ABI), rank-local then summed
     try:
@@ -504,7 +540,7 @@ def main():
         line["fp64_peak_measured_ops_per_s"] = fp64_peak
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if ws > 1:
+    if _dist_on():
         import torch.distributed as dist
         dist.destroy_process_group()
 
