@@ -19,6 +19,7 @@ import numpy as np
 HERE = Path(__file__).resolve().parent
 ROOT = HERE.parent
 LIB = HERE / "liboracle.so"
+QLIB = HERE / "libquad.so"
 DATA = ROOT / "paper_2504_07637_b200" / "data"
 
 _lib = None
@@ -26,10 +27,37 @@ _tables = {}
 
 
 def build(force: bool = False) -> Path:
-    if force or not LIB.exists() or LIB.stat().st_mtime < max(
-            (HERE / f).stat().st_mtime for f in ("boys_oracle.c", "boys_oracle_impl.h")):
+    srcs = ("boys_oracle.c", "boys_oracle_impl.h", "boys_quad.c")
+    newest = max((HERE / f).stat().st_mtime for f in srcs)
+    if force or not LIB.exists() or not QLIB.exists() or min(
+            LIB.stat().st_mtime, QLIB.stat().st_mtime) < newest:
         subprocess.run(["make", "-s", "-C", str(HERE)], check=True)
     return LIB
+
+
+_qlib = None
+
+
+def _quad():
+    global _qlib
+    if _qlib is None:
+        build()
+        Q = C.CDLL(str(QLIB))
+        for f in (Q.boys_quad_downward, Q.boys_ld_downward):
+            f.argtypes = [C.c_int, C.c_void_p, C.c_int64, C.c_void_p]
+        _qlib = Q
+    return _qlib
+
+
+def reference(n: int, x, precision: str = "ld"):
+    """Extended-precision restatement of refmath.boys_downward (oracle/boys_quad.c):
+    F_0..F_n(x) as double-double [N, n+1, 2].  precision 'ld' (x87, ~2^-59,
+    fast) or 'quad' (binary128, ~2^-106)."""
+    xd = np.ascontiguousarray(x, dtype=np.float64).reshape(-1)
+    out = np.empty((xd.size, n + 1, 2))
+    f = _quad().boys_ld_downward if precision == "ld" else _quad().boys_quad_downward
+    f(n, _ptr(xd), xd.size, _ptr(out))
+    return out
 
 
 def lib():
