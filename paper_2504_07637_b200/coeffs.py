@@ -312,8 +312,9 @@ def gen_header(tables: list) -> str:
             vq = ", ".join(f"{{{_lit(y, single)}, {_lit(a, single)}}}" for y, a in row["vq"])
             ul = ", ".join(_lit(y, single) for y in row["ul"])
             vl = ", ".join(_lit(y, single) for y in row["vl"])
+            cn = ", ".join(str(k) for k in kt.counts[kt.orders.index(n)])
             out.append(f"  {{ /* n={n} */ {sc},\n    {{{uq}}},\n    {{{ul}}},\n"
-                       f"    {{{vq}}},\n    {{{vl}}} }},")
+                       f"    {{{vq}}},\n    {{{vl}}},\n    {{{cn}}} }},")
         out.append("};")
         out.append("")
     return "\n".join(out)

@@ -34,6 +34,7 @@
 namespace boys {
 
 constexpr int kThreads = 256;   // points per tile == threads per block
+constexpr int kRaggedFastOrders = 16;
 constexpr unsigned kFull = 0xffffffffu;
 
 static std::atomic<int64_t> g_launches{0};
@@ -66,6 +67,24 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 }
 
 template <typename T> __device__ __forceinline__ T ldg_nc(const T* p) { return __ldg(p); }
+
+// Predicated move / shared store (inline PTX so the compiler keeps plain
+// predication instead of a divergent branch per recursion step).
+__device__ __forceinline__ void pmov(bool p, double& dst, double v) {
+  asm("{ .reg .pred q; setp.ne.b32 q, %2, 0; @q mov.b64 %0, %1; }" : "+d"(dst) : "d"(v), "r"((int)p));
+}
+__device__ __forceinline__ void pmov(bool p, float& dst, float v) {
+  asm("{ .reg .pred q; setp.ne.b32 q, %2, 0; @q mov.b32 %0, %1; }" : "+f"(dst) : "f"(v), "r"((int)p));
+}
+__device__ __forceinline__ void psts(bool p, double* a, double v) {
+  asm volatile("{ .reg .pred q; setp.ne.b32 q, %2, 0; @q st.shared.f64 [%0], %1; }"
+               :: "r"(smem_u32(a)), "d"(v), "r"((int)p) : "memory");
+}
+__device__ __forceinline__ void psts(bool p, float* a, float v) {
+  asm volatile("{ .reg .pred q; setp.ne.b32 q, %2, 0; @q st.shared.f32 [%0], %1; }"
+               :: "r"(smem_u32(a)), "f"(v), "r"((int)p) : "memory");
+}
+
 
 // F_0..F_n for one point, handed to put(m, value) in the order n, n-1, .., 0
 // (then, for lanes past x_up, 0..n again with the upward values).  Returns
@@ -113,7 +132,7 @@ __device__ __forceinline__ void eval_point(T x_in, bool ok, T (&Fv)[n + 1], T& t
 template <typename T, int n, bool AOS, int NBUF, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB)
 dense_kernel(const T* __restrict__ X, int64_t N, T* __restrict__ out, T* __restrict__ expx,
-             int64_t* __restrict__ dom, int64_t index_base, bool bulk_ok) {
+             int64_t* __restrict__ dom, int64_t index_base, bool bulk_ok, bool soa_bulk) {
   constexpr int W = n + 1;
   constexpr int TILE_ELEMS = kThreads * W;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -130,11 +149,33 @@ dense_kernel(const T* __restrict__ X, int64_t N, T* __restrict__ out, T* __restr
     if (in && !ok) flag_domain(dom, index_base + i);
     ok = ok || !in;   // tail lanes evaluate x = 0 quietly
     if constexpr (!AOS) {
-      T* o = out + i;
-      T t = eval_point_stream<T, n>(x, ok, [&](int m, T v) {
-        if (in) __stcs(o + (int64_t)m * N, v);
-      });
-      if (expx && in) __stcs(expx + i, t);
+      if (soa_bulk) {
+        // [n+1][256] tile in shared memory, one bulk copy per order row
+        T* buf = sbase + (it % NBUF) * TILE_ELEMS;
+        if (tid == 0) bulk_wait_read<NBUF - 1>();
+        __syncthreads();
+        T t = eval_point_stream<T, n>(x, ok, [&](int m, T v) { buf[m * kThreads + tid] = v; });
+        if (expx && in) __stcs(expx + i, t);
+        const int64_t cnt = (N - i0) < kThreads ? (N - i0) : kThreads;
+        if (cnt == kThreads) {
+          fence_proxy_async_smem();
+          __syncthreads();
+          if (tid < W) bulk_store(out + (int64_t)tid * N + i0, buf + tid * kThreads,
+                                  kThreads * sizeof(T));
+        } else {
+          __syncthreads();
+          for (int k = tid; k < W * kThreads; k += kThreads) {
+            const int m = k / kThreads, j = k % kThreads;
+            if (j < cnt) __stcs(out + (int64_t)m * N + i0 + j, buf[k]);
+          }
+        }
+      } else {
+        T* o = out + i;
+        T t = eval_point_stream<T, n>(x, ok, [&](int m, T v) {
+          if (in) __stcs(o + (int64_t)m * N, v);
+        });
+        if (expx && in) __stcs(expx + i, t);
+      }
     } else {
       T* buf = sbase + (it % NBUF) * TILE_ELEMS;
       // the slot went to the bulk engine NBUF tiles ago: wait until it was read
@@ -155,29 +196,40 @@ dense_kernel(const T* __restrict__ X, int64_t N, T* __restrict__ out, T* __restr
       }
     }
   }
-  if constexpr (AOS) {
-    if (tid == 0) bulk_wait_all();
+  if (AOS || soa_bulk) {
+    if (tid < (AOS ? 1 : W)) bulk_wait_all();
   }
 }
 
 // ---------------------------------------------------------------------------
 // run-time-order evaluation (ragged / split)
 // ---------------------------------------------------------------------------
-template <typename T>
+// Row accessors for the run-time-order evaluator: rows staged in shared
+// memory (ragged fast path: per-lane orders) or read from __constant__
+// (split: warp-uniform order -> broadcast; rare high-order ragged chunks).
+template <typename T, int R>
 struct SmemTable {
-  BoysRow<T> row[Tab<T>::MAX_ORDER + 1];
-  int shape[Tab<T>::MAX_ORDER + 1][4];
+  BoysRow<T> row[R];
 };
 
-template <typename T>
-__device__ __forceinline__ void stage_table(SmemTable<T>& st) {
-  const int words = sizeof(st.row) / sizeof(T);
-  const T* src = reinterpret_cast<const T*>(&Tab<T>::row(0));
-  T* dst = reinterpret_cast<T*>(&st.row[0]);
+template <typename T, int R>
+__device__ __forceinline__ void stage_table(SmemTable<T, R>& st) {
+  static_assert(sizeof(BoysRow<T>) % sizeof(int) == 0, "row layout");
+  constexpr int words = R * sizeof(BoysRow<T>) / sizeof(int);
+  const int* src = reinterpret_cast<const int*>(&Tab<T>::row(0));
+  int* dst = reinterpret_cast<int*>(&st.row[0]);
   for (int k = threadIdx.x; k < words; k += blockDim.x) dst[k] = src[k];
-  for (int k = threadIdx.x; k < (Tab<T>::MAX_ORDER + 1) * 4; k += blockDim.x)
-    (&st.shape[0][0])[k] = Tab<T>::shape(k / 4, k % 4);
 }
+
+template <typename T>
+struct SmemRows {
+  const BoysRow<T>* p;
+  __device__ __forceinline__ const BoysRow<T>& operator()(int n) const { return p[n]; }
+};
+template <typename T>
+struct ConstRows {
+  __device__ __forceinline__ const BoysRow<T>& operator()(int n) const { return Tab<T>::row(n); }
+};
 
 template <typename T> struct MaxShape;   // compile-time bounds on factor counts
 template <> struct MaxShape<double> {
@@ -211,13 +263,13 @@ template <> struct MaxShape<float> {
 
 // y = x + Q~^{n+1/2} e^{-x} below the cut-off, run-time order; identical
 // operation sequence to seed<T, n>'s Q~ branch.
-template <typename T>
-__device__ __forceinline__ T y_below_rt(T x, T t, int n, const SmemTable<T>& st) {
+template <typename T, typename Rows>
+__device__ __forceinline__ T y_below_rt(T x, T t, int n, const Rows& rows) {
   using A = Ar<T>;
   constexpr int MQ = MaxShape<T>::Q(), ML = MaxShape<T>::L();
-  const BoysRow<T>& R = st.row[n];
-  T u = factored_rt<T, MQ, ML>(x, R.uq, R.ul, st.shape[n][0], st.shape[n][1]);
-  T v = factored_rt<T, MQ, ML>(x, R.vq, R.vl, st.shape[n][2], st.shape[n][3]);
+  const BoysRow<T>& R = rows(n);
+  T u = factored_rt<T, MQ, ML>(x, R.uq, R.ul, R.cnt[0], R.cnt[1]);
+  T v = factored_rt<T, MQ, ML>(x, R.vq, R.vl, R.cnt[2], R.cnt[3]);
   T w = A::div(u, v);
   T h = A::mul(R.q2, w);
   h = A::fma(h, x, R.q1);
@@ -250,15 +302,15 @@ __device__ __forceinline__ T powi_rt_bounded(T b, int n, int bits) {
 // whether the value is one of this lane's outputs (callers store
 // unconditionally to a scratch slot otherwise, so the loop stays branch-free).
 // `wmax` = warp-uniform max order bounds the loops.
-template <typename T, int NB, typename Put>
+template <typename T, int NB, typename Rows, typename Put>
 __device__ __forceinline__ void tail_rt(T x, T y, T t, int n, bool ok, int wmax,
-                                        const SmemTable<T>& st, Put&& put) {
+                                        const Rows& rows, Put&& put) {
   using A = Ar<T>;
   const T bad = A::nan();
   const int bits = 32 - __clz(wmax | 1);
   T r = A::rcp(y);
   T sr = A::sqrt(r);
-  const T c = st.row[n].c;
+  const T c = rows(n).c;
   T cur = n == 0 ? A::mul(c, sr) : A::mul(A::mul(c, powi_rt_bounded(r, n, bits)), sr);
   put(n, ok ? cur : bad, true);
   T tx = A::add(x, x);
@@ -271,7 +323,7 @@ __device__ __forceinline__ void tail_rt(T x, T y, T t, int n, bool ok, int wmax,
       put(m, ok ? cur : bad, on);
     }
   }
-  bool up = ok && x > st.row[n].x_up;
+  bool up = ok && x > rows(n).x_up;
   if (__any_sync(kFull, up)) {
     T rx = A::rcp(x);
     T f = up_first(x);
@@ -286,21 +338,21 @@ __device__ __forceinline__ void tail_rt(T x, T y, T t, int n, bool ok, int wmax,
 }
 
 // Complete run-time-order evaluation (split kernel; ragged fallback tiles).
-template <typename T, int NB, typename Put>
-__device__ __forceinline__ void eval_point_rt(T x_in, bool ok, int n, const SmemTable<T>& st,
+template <typename T, int NB, typename Rows, typename Put>
+__device__ __forceinline__ void eval_point_rt(T x_in, bool ok, int n, const Rows& rows,
                                               Put&& put) {
   using A = Ar<T>;
   T x = ok ? x_in : T(0);
   int ns = ok ? n : 0;
   T t = exp_neg_clamped(x);
-  bool below = ok && x < st.row[ns].z;
+  bool below = ok && x < rows(ns).z;
   T y = x;
   if (__any_sync(kFull, below)) {
-    T yq = y_below_rt(x, t, ns, st);
+    T yq = y_below_rt(x, t, ns, rows);
     y = below ? yq : x;
   }
   int wmax = __reduce_max_sync(kFull, (unsigned)ns);
-  tail_rt<T, NB>(x, y, t, ns, ok, wmax, st, [&](int m, T v, bool on) {
+  tail_rt<T, NB>(x, y, t, ns, ok, wmax, rows, [&](int m, T v, bool on) {
     if (on) put(m, v);
   });
 }
@@ -329,14 +381,14 @@ struct RaggedWarp {
 
 template <typename T, int NB>
 struct RaggedSmem {
-  SmemTable<T> st;
+  SmemTable<T, NB + 1> st;           // rows 0..NB (the fast path's orders)
   RaggedWarp<T, NB> w[kThreads / 32];
 };
 
 // Evaluate up to 32 queued below-cut-off elements (one per lane), writing
 // straight to global memory.
 template <typename T, int NB>
-__device__ __forceinline__ void ragged_drain(RaggedWarp<T, NB>& W, const SmemTable<T>& st,
+__device__ __forceinline__ void ragged_drain(RaggedWarp<T, NB>& W, const SmemRows<T>& st,
                                              int& qn, int lane, T* __restrict__ out) {
   // queued elements' slots were written (with stale staging data) by earlier
   // bulk stores of their chunks: those must be complete before we overwrite
@@ -381,6 +433,7 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
   RaggedSmem<T, NB>& S = *reinterpret_cast<RaggedSmem<T, NB>*>(smem_raw);
   stage_table(S.st);
   __syncthreads();
+  const SmemRows<T> rows{S.st.row};
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   RaggedWarp<T, NB>& W = S.w[wid];
   const int64_t nchunks = (N + 31) / 32;
@@ -411,17 +464,20 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
     const int n = pn;
     const int64_t goff = poff, base = pbase, cnt = plast_off - pbase;
     load(c + wstride);
+    constexpr int MAXN = Tab<T>::MAX_ORDER;
     const bool xok = valid_x(x);
-    if (in && !(xok && n <= NB)) flag_domain(dom, i);
+    if (in && !(xok && n <= MAXN)) flag_domain(dom, i);
     if (__any_sync(kFull, in && n > NB)) {
-      // an order above the table: every lane writes its own values directly
-      if (in && n > NB) {
+      // an order above the fast path's bound: every lane evaluates its own
+      // element from the __constant__ rows and writes it directly (NaN for
+      // orders above the table)
+      if (in && n > MAXN) {
         for (int m = 0; m <= n; ++m) out[goff + m] = A::nan();
       }
-      const bool okl = in && xok && n <= NB;
+      const bool okl = in && xok && n <= MAXN;
       T* dst = out + goff;
-      eval_point_rt<T, NB>(x, okl, okl ? n : 0, S.st, [&](int m, T v) {
-        if (in && n <= NB) dst[m] = v;
+      eval_point_rt<T, MAXN>(x, okl, okl ? n : 0, ConstRows<T>{}, [&](int m, T v) {
+        if (in && n <= MAXN) dst[m] = v;
       });
       continue;
     }
@@ -429,7 +485,7 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
     const T xs = ok ? x : A::nan();                // NaN propagates through the tail
     const T xe = ok ? x : T(0);
     const T t = exp_neg_clamped(xe);
-    const bool defer = ok && xe < S.st.row[n].z;
+    const bool defer = ok && xe < rows(n).z;
     const unsigned dmask = __ballot_sync(kFull, defer);
     // staging position matches the global 16-byte phase of the chunk range
     constexpr int Q = 16 / sizeof(T);
@@ -457,20 +513,20 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
       const int bits = 32 - __clz(wmax | 1);
       const T r = A::rcp(xs);
       const T sr = A::sqrt(r);
-      const T cn = S.st.row[n].c;
+      const T cn = rows(n).c;
       T cur = n == 0 ? A::mul(cn, sr) : A::mul(A::mul(cn, powi_rt_bounded(r, n, bits)), sr);
       if (wr) dst[n] = cur;
       const T tx = A::add(xs, xs);
 #pragma unroll
       for (int m = NB - 1; m >= 0; --m) {
         if (m < wmax) {                            // warp-uniform
-          if (m < n) {                             // predicated, no select
-            cur = A::mul(A::fma(tx, cur, t), rinv<T>(m));
-            if (wr) dst[m] = cur;
-          }
+          const T nx = A::mul(A::fma(tx, cur, t), rinv<T>(m));
+          const bool on = m < n;
+          pmov(on, cur, nx);                       // predicated, branch-free
+          psts(on && wr, dst + m, cur);
         }
       }
-      const bool up = wr && ok && xs > S.st.row[n].x_up;
+      const bool up = wr && ok && xs > rows(n).x_up;
       if (__any_sync(kFull, up)) {
         const T rx = A::rcp(xs);
         T f = up_first(xs);
@@ -500,9 +556,9 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
         if (lane == 0) bulk_store(out + base + head, W.stage + shift + head, body * sizeof(T));
       }
     }
-    if (qn >= 32) ragged_drain<T, NB>(W, S.st, qn, lane, out);
+    if (qn >= 32) ragged_drain<T, NB>(W, rows, qn, lane, out);
   }
-  while (qn > 0) ragged_drain<T, NB>(W, S.st, qn, lane, out);
+  while (qn > 0) ragged_drain<T, NB>(W, rows, qn, lane, out);
   if (lane == 0) bulk_wait_all();
 }
 
@@ -515,9 +571,6 @@ __global__ void __launch_bounds__(kThreads)
 split_kernel(const T* __restrict__ X, int64_t N, int nbar, T* __restrict__ out,
              int64_t* __restrict__ dom) {
   constexpr int W = n + 1;
-  __shared__ SmemTable<T> st;
-  stage_table(st);
-  __syncthreads();
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < N; i0 += stride) {
     const int64_t i = i0 + threadIdx.x;
@@ -531,7 +584,7 @@ split_kernel(const T* __restrict__ X, int64_t N, int nbar, T* __restrict__ out,
     eval_point_stream<T, n>(x, ok, [&](int m, T v) {
       if (in && m > nbar) __stcs(o + m * stride_m, v);
     });
-    eval_point_rt<T, n>(x, ok, nbar, st, [&](int m, T v) {
+    eval_point_rt<T, n>(x, ok, nbar, ConstRows<T>{}, [&](int m, T v) {
       if (in && m <= nbar) __stcs(o + m * stride_m, v);
     });
   }
@@ -635,6 +688,10 @@ static int aos_nbuf() {
   static int v = env_int("BOYS_AOS_NBUF", 2) == 1 ? 1 : 2;
   return v;
 }
+static int soa_tma() {   // BOYS_SOA_TMA=1: SoA rows leave as bulk copies
+  static int v = env_int("BOYS_SOA_TMA", 0);
+  return v;
+}
 static int aos_minb() {
   static int v = env_int("BOYS_AOS_MINB", 4) == 6 ? 6 : 4;
   return v;
@@ -644,16 +701,21 @@ template <typename T, int n, bool AOS, int NBUF, int MINB>
 static boys_status launch_dense_k(const T* x, int64_t N, T* out, T* expx, int64_t* dom,
                                   int64_t base, cudaStream_t s) {
   auto k = dense_kernel<T, n, AOS, NBUF, MINB>;
-  size_t smem = AOS ? (size_t)NBUF * kThreads * (n + 1) * sizeof(T) : 0;
-  static bool attr = false;   // per instantiation
+  // SoA bulk rows need every row start 16-byte aligned: N * sizeof(T) % 16 == 0
+  const bool soa_bulk = !AOS && soa_tma() && (N * (int64_t)sizeof(T)) % 16 == 0 &&
+                        (reinterpret_cast<uintptr_t>(out) % 16) == 0;
+  size_t smem = (AOS || soa_bulk) ? (size_t)NBUF * kThreads * (n + 1) * sizeof(T) : 0;
+  static bool attr = false;   // per instantiation; sized for the largest use
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int smem_max = (int)((size_t)NBUF * kThreads * (n + 1) * sizeof(T));
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);
     if (e != cudaSuccess) return cuda_status(e);
     attr = true;
   }
   int64_t ntiles = (N + kThreads - 1) / kThreads;
   bool bulk_ok = (reinterpret_cast<uintptr_t>(out) % 16) == 0;
-  k<<<blocks_for(k, smem, ntiles), kThreads, smem, s>>>(x, N, out, expx, dom, base, bulk_ok);
+  k<<<blocks_for(k, smem, ntiles), kThreads, smem, s>>>(x, N, out, expx, dom, base, bulk_ok,
+                                                        soa_bulk);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cuda_status(cudaGetLastError());
 }
@@ -662,9 +724,14 @@ template <typename T, int n, bool AOS>
 static boys_status launch_dense_t(const T* x, int64_t N, T* out, T* expx, int64_t* dom,
                                   int64_t base, cudaStream_t s) {
   if constexpr (!AOS) {
+    constexpr bool fits2 = 2 * kThreads * (n + 1) * sizeof(T) <= 80 * 1024;
+    if (soa_tma()) return launch_dense_k<T, n, false, (fits2 ? 2 : 1), 4>(x, N, out, expx, dom, base, s);
     return launch_dense_k<T, n, false, 1, (n <= 1 ? 8 : 4)>(x, N, out, expx, dom, base, s);
   } else {
-    if (aos_nbuf() == 2) return launch_dense_k<T, n, true, 2, 4>(x, N, out, expx, dom, base, s);
+    // double-buffer the AoS tile while two tiles fit in ~80 KB (n <= 18 in f64)
+    constexpr bool fits2 = 2 * kThreads * (n + 1) * sizeof(T) <= 80 * 1024;
+    if (fits2 && aos_nbuf() == 2)
+      return launch_dense_k<T, n, true, (fits2 ? 2 : 1), 4>(x, N, out, expx, dom, base, s);
     if (aos_minb() == 6) return launch_dense_k<T, n, true, 1, 6>(x, N, out, expx, dom, base, s);
     return launch_dense_k<T, n, true, 1, 4>(x, N, out, expx, dom, base, s);
   }
@@ -723,7 +790,9 @@ static boys_status dispatch_split(int nn, int nbar, const void* x, int64_t N, vo
 template <typename T>
 static boys_status launch_ragged(const void* x, const uint8_t* nm, const int64_t* off, int64_t N,
                                  void* out, int64_t* dom, cudaStream_t s) {
-  constexpr int NB = Tab<T>::MAX_ORDER;
+  // fast-path order bound (staging per warp = 32 x (NB+1) values); higher
+  // orders, up to the table maximum, take the in-kernel fallback path
+  constexpr int NB = Tab<T>::MAX_ORDER < kRaggedFastOrders ? Tab<T>::MAX_ORDER : kRaggedFastOrders;
   auto k = ragged_kernel<T, NB>;
   const size_t smem = sizeof(RaggedSmem<T, NB>);
   static bool attr = false;

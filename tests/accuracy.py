@@ -16,13 +16,23 @@ TABLE1_F64 = {
     6: (48.3, 48.3, 47.0, 51.1), 7: (48.1, 48.3, 46.6, 51.3), 8: (48.2, 48.2, 46.2, 51.0),
     9: (47.8, 47.9, 45.5, 50.1), 10: (47.6, 47.5, 45.4, 49.3), 11: (47.8, 47.4, 45.0, 51.0),
     12: (47.6, 47.4, 44.6, 50.7), 13: (47.4, 47.2, 44.8, 50.3), 14: (47.3, 47.0, 44.5, 49.9),
-    15: (47.1, 46.5, 43.9, 49.6), 16: (47.0, 46.6, 44.1, 49.2),
+    15: (47.1, 46.5, 43.9, 49.6), 16: (47.0, 46.6, 44.1, 49.2), 17: (47.0, 46.4, 43.8, 48.8),
+    18: (47.4, 46.2, 43.4, 51.6), 19: (47.2, 46.1, 43.2, 51.3), 20: (47.1, 46.0, 43.3, 51.1),
+    21: (47.1, 45.7, 43.1, 50.8), 22: (47.0, 45.8, 43.2, 50.5), 23: (46.8, 45.6, 42.8, 50.3),
+    24: (46.7, 45.6, 42.9, 50.1), 25: (46.5, 45.6, 43.0, 49.9), 26: (46.7, 45.0, 42.4, 49.7),
+    27: (46.6, 45.5, 42.7, 49.5), 28: (46.4, 45.1, 42.3, 49.3), 29: (46.4, 45.1, 42.3, 49.1),
+    30: (46.4, 45.1, 42.2, 48.9), 31: (46.3, 44.5, 41.8, 48.8), 32: (46.3, 44.9, 42.2, 48.6),
+    33: (46.3, 44.4, 41.8, 48.4), 34: (46.3, 44.6, 41.8, 48.3), 35: (46.1, 44.3, 41.5, 48.2),
+    36: (46.0, 44.3, 41.8, 48.0),
 }
 # 24-bit single half of Table I
 TABLE1_F32 = {
     0: (22.9, None, 22.9, 27.3), 1: (21.4, None, 21.1, 23.7), 2: (21.0, 21.1, 19.8, 27.3),
     3: (20.4, 20.4, 19.0, 25.5), 4: (20.1, 20.2, 18.5, 24.2), 5: (19.8, 20.0, 18.3, 23.3),
     6: (19.4, 19.5, 17.7, 22.5), 7: (19.2, 19.4, 17.5, 21.9), 8: (19.0, 19.0, 17.0, 21.3),
+    9: (18.9, 18.8, 16.7, 20.9), 10: (18.9, 18.7, 16.4, 24.9), 11: (19.2, 18.6, 16.1, 24.5),
+    12: (18.6, 18.4, 16.1, 24.2), 13: (18.5, 18.3, 15.9, 23.8), 14: (18.4, 18.1, 15.7, 23.5),
+    15: (18.5, 17.8, 15.1, 23.3), 16: (18.4, 17.7, 15.3, 23.0),
 }
 SLACK = 2.0   # SPEC.md:424-426 ("within 2 bits")
 

@@ -94,8 +94,8 @@ def main():
     d64, d32 = load_ds("double53"), load_ds("single24")
     with mp_.Pool(a.procs) as pool:
         # ---- Table-I scans --------------------------------------------------
-        for tag, ds, orders, dtype in (("f64", d64, (0, 2, 5, 8, 12, 16), np.float64),
-                                       ("f32", d32, (0, 5, 8), np.float32)):
+        for tag, ds, orders, dtype in (("f64", d64, (0, 2, 5, 8, 12, 16, 24, 36), np.float64),
+                                       ("f32", d32, (0, 5, 8, 16), np.float32)):
             blob = {}
             for n in orders:
                 z = ds.records[n].z
