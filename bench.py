@@ -511,7 +511,9 @@ def main():
         extras = {}
         del wl
         torch.cuda.empty_cache()
-        flushbuf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+        # 1 GiB (8x L2): flushes L2 and keeps the GPU busy long enough that
+        # the host has enqueued the next launch before the timed event fires
+        flushbuf = torch.empty(1 << 30, dtype=torch.uint8, device=dev)
         for name in ("cfg1", "cfg2", "cfg4", "cfg4f32", "cfg5"):
             if name == args.config:
                 continue
@@ -528,7 +530,7 @@ def main():
                                 "gpu_launches": l2,
                                 "roofline": roofline_obj(w2, p2, hbm_peak, fp64_peak,
                                                          traffic=committed_traffic(name)),
-                                "l2": "flushed (256 MiB memset) before every launch; "
+                                "l2": "flushed (1 GiB memset) before every launch; "
                                       "kernel time only" if small else "exceeds L2"}
                 del w2
                 torch.cuda.empty_cache()

@@ -667,11 +667,21 @@ static boys_status cuda_status(cudaError_t e) {
 
 // Persistent grid: SMs x resident blocks (measured better than one block per
 // tile even for the 2^20-point config: block launch overhead dominates there).
+// The occupancy query is cached per (kernel, shared-memory size): it is a
+// host-side call that would otherwise sit on every launch's critical path.
 template <typename K>
 static int blocks_for(K kernel, size_t smem, int64_t ntiles) {
+  static thread_local struct { const void* k; size_t smem; int occ; } cache[8] = {};
+  const void* key = reinterpret_cast<const void*>(kernel);
   int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, smem);
-  if (occ < 1) occ = 1;
+  for (auto& c : cache)
+    if (c.k == key && c.smem == smem) { occ = c.occ; break; }
+  if (!occ) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, smem);
+    if (occ < 1) occ = 1;
+    for (auto& c : cache)
+      if (!c.k) { c = {key, smem, occ}; break; }
+  }
   int64_t b = (int64_t)sm_count() * occ;
   if (ntiles < b) b = ntiles;
   return (int)(b < 1 ? 1 : b);
@@ -690,6 +700,10 @@ static int aos_nbuf() {
 }
 static int soa_tma() {   // BOYS_SOA_TMA=1: SoA rows leave as bulk copies
   static int v = env_int("BOYS_SOA_TMA", 0);
+  return v;
+}
+static int soa_small_minb() {   // BOYS_SOA0_MINB: 8 (default) or 6 for n <= 1
+  static int v = env_int("BOYS_SOA0_MINB", 8) == 6 ? 6 : 8;
   return v;
 }
 static int aos_minb() {
@@ -726,6 +740,9 @@ static boys_status launch_dense_t(const T* x, int64_t N, T* out, T* expx, int64_
   if constexpr (!AOS) {
     constexpr bool fits2 = 2 * kThreads * (n + 1) * sizeof(T) <= 80 * 1024;
     if (soa_tma()) return launch_dense_k<T, n, false, (fits2 ? 2 : 1), 4>(x, N, out, expx, dom, base, s);
+    if constexpr (n <= 1) {          // small orders: register budget for 6 or 8 blocks/SM
+      if (soa_small_minb() == 6) return launch_dense_k<T, n, false, 1, 6>(x, N, out, expx, dom, base, s);
+    }
     return launch_dense_k<T, n, false, 1, (n <= 1 ? 8 : 4)>(x, N, out, expx, dom, base, s);
   } else {
     // double-buffer the AoS tile while two tiles fit in ~80 KB (n <= 18 in f64)
