@@ -38,8 +38,10 @@ def load(build_if_missing: bool = True) -> C.CDLL:
     with _lock:
         if _lib is not None:
             return _lib
-        path = _build.LIB
-        if build_if_missing and _build.stale():
+        import os
+        override = os.environ.get("BOYS_LIB")      # experiments: an alternative build
+        path = _build.LIB if not override else __import__("pathlib").Path(override)
+        if not override and build_if_missing and _build.stale():
             try:
                 _build.build_libboys()
             except Exception as e:   # noqa: BLE001

@@ -35,6 +35,9 @@ namespace boys {
 
 constexpr int kThreads = 256;   // points per tile == threads per block
 constexpr int kRaggedFastOrders = 16;
+#ifndef BOYS_SOA_MINB
+#define BOYS_SOA_MINB 4   // SoA resident-block target (register budget 64/thread)
+#endif
 constexpr unsigned kFull = 0xffffffffu;
 
 static std::atomic<int64_t> g_launches{0};
@@ -563,264 +566,6 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
 }
 
 // ---------------------------------------------------------------------------
-// ragged kernel, order-sorted super-chunks (SC chunks of 32 per warp step).
-// Same per-element arithmetic as ragged_kernel; the immediate elements of a
-// super-chunk are counting-sorted by order in warp-private shared memory and
-// processed in rounds of 32, so each round's recursion and exponentiation run
-// to that round's (small, nearly uniform) orders instead of the chunk max.
-// Super-chunks whose output exceeds the staging capacity are processed as SC
-// plain chunks (unsorted), those holding an order above NB per element.
-// ---------------------------------------------------------------------------
-template <typename T, int NB, int SC>
-struct RaggedSCWarp {
-  static constexpr int E = 32 * SC;
-  static constexpr int CAP = (E * 6 > 32 * (NB + 1)) ? E * 6 : 32 * (NB + 1);
-  alignas(16) T stage[CAP + 16 / sizeof(T)];
-  T ex[E], et[E];
-  int eloc[E];
-  unsigned char en[E], perm[E];
-  int hist[NB + 2];
-  // deferred queue: at most 31 carried over + E enqueued within one
-  // super-chunk, so it never drains mid-super-chunk (a drained element of the
-  // current super-chunk would be overwritten by its range's bulk store)
-  static constexpr int QCAP = 32 + E;
-  T qx[QCAP], qt[QCAP];
-  int64_t qoff[QCAP];
-  unsigned char qn[QCAP];
-  T scratch[32];
-};
-
-template <typename T, int NB, int SC>
-struct RaggedSCSmem {
-  SmemTable<T, NB + 1> st;
-  RaggedSCWarp<T, NB, SC> w[kThreads / 32];
-};
-
-// immediate tail (past the cut-off, y = x) for one element per lane into the
-// staging slot dst (same operation sequence as seed<T,n> + recursion + ladder)
-template <typename T, int NB>
-__device__ __forceinline__ void imm_tail(T xs, T t, int n, bool wr, int wmax,
-                                         const SmemRows<T>& rows, T* dst) {
-  using A = Ar<T>;
-  const int bits = 32 - __clz(wmax | 1);
-  const T r = A::rcp(xs);
-  const T sr = A::sqrt(r);
-  const T cn = rows(n).c;
-  T cur = n == 0 ? A::mul(cn, sr) : A::mul(A::mul(cn, powi_rt_bounded(r, n, bits)), sr);
-  if (wr) dst[n] = cur;
-  const T tx = A::add(xs, xs);
-#pragma unroll
-  for (int m = NB - 1; m >= 0; --m) {
-    if (m < wmax) {                            // warp-uniform
-      const T nx = A::mul(A::fma(tx, cur, t), rinv<T>(m));
-      const bool on = m < n;
-      pmov(on, cur, nx);
-      psts(on && wr, dst + m, cur);
-    }
-  }
-  const bool up = wr && xs > rows(n).x_up;     // NaN xs (invalid lanes) -> false
-  if (__any_sync(kFull, up)) {
-    const T rx = A::rcp(xs);
-    T f = up_first(xs);
-    if (up) dst[0] = f;
-#pragma unroll
-    for (int m = 0; m < NB; ++m) {
-      if (m >= wmax) break;
-      f = up_next(f, m, rx);
-      if (up && m + 1 <= n) dst[m + 1] = f;
-    }
-  }
-}
-
-// staged range [base, base+cnt) -> global: scalar head/tail, bulk body
-template <typename T>
-__device__ __forceinline__ void range_store(const T* stage, int shift, int64_t base, int cnt,
-                                            int lane, T* __restrict__ out) {
-  constexpr int Q = 16 / sizeof(T);
-  const int head = ((Q - shift) & (Q - 1)) < cnt ? ((Q - shift) & (Q - 1)) : cnt;
-  const int body = ((cnt - head) / Q) * Q;
-  const int tail0 = head + body;
-  if (lane < head) __stcs(out + base + lane, stage[shift + lane]);
-  if (lane < cnt - tail0) __stcs(out + base + tail0 + lane, stage[shift + tail0 + lane]);
-  if (body > 0) {
-    fence_proxy_async_smem();
-    __syncwarp();
-    if (lane == 0) bulk_store(out + base + head, stage + shift + head, body * sizeof(T));
-  }
-}
-
-template <typename T, int NB, int SC>
-__device__ __forceinline__ void ragged_sc_drain(RaggedSCWarp<T, NB, SC>& W,
-                                                const SmemRows<T>& rows, int& qn, int lane,
-                                                T* __restrict__ out) {
-  if (lane == 0) bulk_wait_all();
-  __syncwarp();
-  const int take = qn < 32 ? qn : 32;
-  const bool has = lane < take;
-  const int slot = qn - take + lane;
-  const T x = has ? W.qx[slot] : T(0);
-  const T t = has ? W.qt[slot] : T(0);
-  const int n = has ? (int)W.qn[slot] : 0;
-  const int64_t off = has ? W.qoff[slot] : 0;
-  __syncwarp();
-  const T y = has ? y_below_rt(x, t, n, rows) : x;
-  const int wmax = __reduce_max_sync(kFull, (unsigned)n);
-  T* dst = out + off;
-  T* sink = W.scratch + lane;
-  tail_rt<T, NB>(x, y, t, n, has, wmax, rows,
-                 [&](int m, T v, bool on) { *((has && on) ? dst + m : sink) = v; });
-  qn -= take;
-}
-
-template <typename T, int NB, int SC>
-__global__ void __launch_bounds__(kThreads)
-ragged_sc_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
-                 const int64_t* __restrict__ OFF, int64_t N, T* __restrict__ out,
-                 int64_t* __restrict__ dom) {
-  using A = Ar<T>;
-  using WS = RaggedSCWarp<T, NB, SC>;
-  constexpr int E = WS::E, CAP = WS::CAP, Q = 16 / sizeof(T), MAXN = Tab<T>::MAX_ORDER;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  RaggedSCSmem<T, NB, SC>& S = *reinterpret_cast<RaggedSCSmem<T, NB, SC>*>(smem_raw);
-  stage_table(S.st);
-  __syncthreads();
-  const SmemRows<T> rows{S.st.row};
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  WS& W = S.w[wid];
-  const unsigned lt = (1u << lane) - 1u;
-  const int64_t nsc = (N + E - 1) / E;
-  const int64_t wstride = (int64_t)gridDim.x * (kThreads / 32);
-  int qn = 0;
-  for (int64_t sc = (int64_t)blockIdx.x * (kThreads / 32) + wid; sc < nsc; sc += wstride) {
-    const int64_t e0 = sc * E;
-    const int64_t elast = (e0 + E < N) ? e0 + E : N;
-    const int64_t base = __ldg(OFF + e0);
-    const int64_t cnt = __ldg(OFF + elast) - base;
-    T x[SC];
-    int n[SC];
-    int64_t goff[SC];
-    bool in[SC];
-    bool hi = false;
-#pragma unroll
-    for (int r = 0; r < SC; ++r) {
-      const int64_t i = e0 + r * 32 + lane;
-      in[r] = i < N;
-      x[r] = in[r] ? ldg_nc(X + i) : T(0);
-      n[r] = in[r] ? (int)NM[i] : 0;
-      goff[r] = in[r] ? __ldg(OFF + i) : 0;
-      if (in[r] && !(valid_x(x[r]) && n[r] <= MAXN)) flag_domain(dom, i);
-      hi = hi || (in[r] && n[r] > NB);
-    }
-    if (__any_sync(kFull, hi)) {
-      // an order above the fast path: per-element evaluation, direct writes
-#pragma unroll
-      for (int r = 0; r < SC; ++r) {
-        if (in[r] && n[r] > MAXN) {
-          for (int m = 0; m <= n[r]; ++m) out[goff[r] + m] = A::nan();
-        }
-        const bool okl = in[r] && valid_x(x[r]) && n[r] <= MAXN;
-        T* dst = out + goff[r];
-        const bool wr = in[r] && n[r] <= MAXN;
-        eval_point_rt<T, MAXN>(x[r], okl, okl ? n[r] : 0, ConstRows<T>{},
-                               [&](int m, T v) { if (wr) dst[m] = v; });
-      }
-      continue;
-    }
-    // the previous range's bulk store must have finished reading the staging
-    if (lane == 0) bulk_wait_read<0>();
-    __syncwarp();
-    const bool sorted = cnt + Q <= CAP;
-    const int shift = sorted ? (int)(base & (Q - 1)) : 0;
-    if (lane < NB + 2) W.hist[lane] = 0;
-    __syncwarp();
-    int key[SC], rank[SC];
-#pragma unroll
-    for (int r = 0; r < SC; ++r) {
-      const bool ok = in[r] && valid_x(x[r]);
-      const T xs = ok ? x[r] : A::nan();
-      const T xe = ok ? x[r] : T(0);
-      const T t = exp_neg_clamped(xe);
-      const bool defer = ok && xe < rows(n[r]).z;
-      const unsigned dmask = __ballot_sync(kFull, defer);
-      if (dmask) {                                   // enqueue (qn stays warp-uniform)
-        if (defer) {
-          const int slot = qn + __popc(dmask & lt);
-          W.qx[slot] = xe;
-          W.qt[slot] = t;
-          W.qn[slot] = (unsigned char)n[r];
-          W.qoff[slot] = goff[r];
-        }
-        qn += __popc(dmask);
-        __syncwarp();
-      }
-      const int slot = r * 32 + lane;
-      W.ex[slot] = xs;
-      W.et[slot] = t;
-      W.en[slot] = (unsigned char)n[r];
-      W.eloc[slot] = (int)(goff[r] - base) + shift;
-      key[r] = (in[r] && !defer) ? n[r] : NB + 1;
-      // rank within the order bucket (warp-aggregated shared-memory atomics)
-      const unsigned peers = __match_any_sync(kFull, key[r]);
-      const int leader = __ffs(peers) - 1;
-      int b0 = 0;
-      if (lane == leader) b0 = atomicAdd(&W.hist[key[r]], __popc(peers));
-      rank[r] = __shfl_sync(kFull, b0, leader) + __popc(peers & lt);
-    }
-    __syncwarp();
-    if (sorted) {
-      // exclusive scan of the bucket counts (NB + 2 <= 32 lanes)
-      const int h = lane < NB + 2 ? W.hist[lane] : 0;
-      int v = h;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const int o = __shfl_up_sync(kFull, v, d);
-        if (lane >= d) v += o;
-      }
-      const int nimm = __shfl_sync(kFull, v - h, NB + 1);   // start of the skip bucket
-      __syncwarp();
-      if (lane < NB + 2) W.hist[lane] = v - h;
-      __syncwarp();
-#pragma unroll
-      for (int r = 0; r < SC; ++r)
-        if (key[r] <= NB) W.perm[W.hist[key[r]] + rank[r]] = (unsigned char)(r * 32 + lane);
-      __syncwarp();
-      for (int q0 = 0; q0 < nimm; q0 += 32) {       // rounds of 32, orders ascending
-        const int p = q0 + lane;
-        const bool has = p < nimm;
-        const int e = has ? W.perm[p] : 0;
-        const int ne = has ? (int)W.en[e] : 0;
-        const int wmax = __reduce_max_sync(kFull, (unsigned)ne);
-        imm_tail<T, NB>(W.ex[e], W.et[e], ne, has, wmax, rows, W.stage + (has ? W.eloc[e] : 0));
-      }
-      __syncwarp();
-      range_store(W.stage, shift, base, (int)cnt, lane, out);
-    } else {
-      // output beyond the staging capacity: plain chunks, unsorted
-#pragma unroll
-      for (int r = 0; r < SC; ++r) {
-        const int64_t c0 = e0 + r * 32;
-        if (c0 >= N) break;
-        const int64_t cl = (c0 + 32 < N) ? c0 + 32 : N;
-        const int64_t cb = __ldg(OFF + c0), cc = __ldg(OFF + cl) - cb;
-        const int csh = (int)(cb & (Q - 1));
-        if (lane == 0) bulk_wait_read<0>();
-        __syncwarp();
-        const int slot = r * 32 + lane;
-        const bool wr = key[r] <= NB;
-        const int wmax = __reduce_max_sync(kFull, (unsigned)(wr ? n[r] : 0));
-        imm_tail<T, NB>(W.ex[slot], W.et[slot], W.en[slot], wr, wmax, rows,
-                        W.stage + (int)(goff[r] - cb) + csh);
-        __syncwarp();
-        range_store(W.stage, csh, cb, (int)cc, lane, out);
-      }
-    }
-    while (qn >= 32) ragged_sc_drain<T, NB, SC>(W, rows, qn, lane, out);
-  }
-  while (qn > 0) ragged_sc_drain<T, NB, SC>(W, rows, qn, lane, out);
-  if (lane == 0) bulk_wait_all();
-}
-
-// ---------------------------------------------------------------------------
 // split kernel (eval_with_split): F_m for m <= nbar equals a
 // dense order-nbar evaluation, F_m for m > nbar a dense order-n evaluation.
 // ---------------------------------------------------------------------------
@@ -1001,7 +746,7 @@ static boys_status launch_dense_t(const T* x, int64_t N, T* out, T* expx, int64_
     if constexpr (n <= 1) {          // small orders: register budget for 6 or 8 blocks/SM
       if (soa_small_minb() == 6) return launch_dense_k<T, n, false, 1, 6>(x, N, out, expx, dom, base, s);
     }
-    return launch_dense_k<T, n, false, 1, (n <= 1 ? 8 : 4)>(x, N, out, expx, dom, base, s);
+    return launch_dense_k<T, n, false, 1, (n <= 1 ? 8 : BOYS_SOA_MINB)>(x, N, out, expx, dom, base, s);
   } else {
     // double-buffer the AoS tile while two tiles fit in ~80 KB (n <= 18 in f64)
     constexpr bool fits2 = 2 * kThreads * (n + 1) * sizeof(T) <= 80 * 1024;
@@ -1071,44 +816,21 @@ static boys_status set_smem(K k, size_t smem, bool& done) {
   return BOYS_OK;
 }
 
-static int ragged_sc() {   // BOYS_RAGGED_SC: chunks per sorted super-chunk (1 = unsorted)
-  static int v = [] {
-    int k = env_int("BOYS_RAGGED_SC", 2);
-    return (k == 1 || k == 4) ? k : 2;
-  }();
-  return v;
-}
-
 template <typename T>
 static boys_status launch_ragged(const void* x, const uint8_t* nm, const int64_t* off, int64_t N,
                                  void* out, int64_t* dom, cudaStream_t s) {
   // fast-path order bound (staging per warp = 32 x (NB+1) values); higher
-  // orders, up to the table maximum, take the in-kernel fallback path
+  // orders, up to the table maximum, take the in-kernel fallback path.
+  // (Order-sorted super-chunks of 64/128 elements were measured slower on
+  // B200: 2.90 / 3.79 ms vs 2.42 ms for cfg4 -- more registers and smem.)
   constexpr int NB = Tab<T>::MAX_ORDER < kRaggedFastOrders ? Tab<T>::MAX_ORDER : kRaggedFastOrders;
-  const int sc = ragged_sc();
-  boys_status st = BOYS_OK;
-  if (sc == 1) {
-    auto k = ragged_kernel<T, NB>;
-    const size_t smem = sizeof(RaggedSmem<T, NB>);
-    static bool done = false;
-    if ((st = set_smem(k, smem, done)) != BOYS_OK) return st;
-    const int64_t nch = (N + 31) / 32;
-    k<<<blocks_for(k, smem, (nch + 7) / 8), kThreads, smem, s>>>((const T*)x, nm, off, N, (T*)out, dom);
-  } else if (sc == 2) {
-    auto k = ragged_sc_kernel<T, NB, 2>;
-    const size_t smem = sizeof(RaggedSCSmem<T, NB, 2>);
-    static bool done = false;
-    if ((st = set_smem(k, smem, done)) != BOYS_OK) return st;
-    const int64_t nsc = (N + 63) / 64;
-    k<<<blocks_for(k, smem, (nsc + 7) / 8), kThreads, smem, s>>>((const T*)x, nm, off, N, (T*)out, dom);
-  } else {
-    auto k = ragged_sc_kernel<T, NB, 4>;
-    const size_t smem = sizeof(RaggedSCSmem<T, NB, 4>);
-    static bool done = false;
-    if ((st = set_smem(k, smem, done)) != BOYS_OK) return st;
-    const int64_t nsc = (N + 127) / 128;
-    k<<<blocks_for(k, smem, (nsc + 7) / 8), kThreads, smem, s>>>((const T*)x, nm, off, N, (T*)out, dom);
-  }
+  auto k = ragged_kernel<T, NB>;
+  const size_t smem = sizeof(RaggedSmem<T, NB>);
+  static bool done = false;
+  boys_status st = set_smem(k, smem, done);
+  if (st != BOYS_OK) return st;
+  const int64_t nch = (N + 31) / 32;
+  k<<<blocks_for(k, smem, (nch + 7) / 8), kThreads, smem, s>>>((const T*)x, nm, off, N, (T*)out, dom);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cuda_status(cudaGetLastError());
 }
