@@ -705,6 +705,10 @@ static int soa_tma() {   // BOYS_SOA_TMA=1: SoA rows leave as bulk copies
   static int v = env_int("BOYS_SOA_TMA", 0);
   return v;
 }
+static int grid_tiles() {
+  static int v = env_int("BOYS_GRID_TILES", 0);
+  return v;
+}
 static int soa_small_minb() {   // BOYS_SOA0_MINB: 8 (default) or 6 for n <= 1
   static int v = env_int("BOYS_SOA0_MINB", 8) == 6 ? 6 : 8;
   return v;
@@ -731,8 +735,11 @@ static boys_status launch_dense_k(const T* x, int64_t N, T* out, T* expx, int64_
   }
   int64_t ntiles = (N + kThreads - 1) / kThreads;
   bool bulk_ok = (reinterpret_cast<uintptr_t>(out) % 16) == 0;
-  k<<<blocks_for(k, smem, ntiles), kThreads, smem, s>>>(x, N, out, expx, dom, base, bulk_ok,
-                                                        soa_bulk);
+  // BOYS_GRID_TILES=1: one block per tile (the block scheduler balances the
+  // tail) instead of the persistent grid -- A/B knob for small batches
+  int grid = blocks_for(k, smem, ntiles);
+  if (grid_tiles() && ntiles <= (int64_t)1 << 30) grid = (int)ntiles;
+  k<<<grid, kThreads, smem, s>>>(x, N, out, expx, dom, base, bulk_ok, soa_bulk);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cuda_status(cudaGetLastError());
 }
