@@ -670,6 +670,21 @@ static boys_status cuda_status(cudaError_t e) {
 
 // Persistent grid: SMs x resident blocks (measured better than one block per
 // tile even for the 2^20-point config: block launch overhead dominates there).
+// Opt a kernel in to more than 48 KB of dynamic shared memory on the current
+// device (the attribute is per device; `mask` remembers which devices are done).
+template <typename K>
+static boys_status opt_in_smem(K kernel, int smem, std::atomic<uint64_t>& mask) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_status(e);
+  const uint64_t bit = uint64_t(1) << (dev & 63);
+  if (mask.load(std::memory_order_acquire) & bit) return BOYS_OK;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return cuda_status(e);
+  mask.fetch_or(bit, std::memory_order_acq_rel);
+  return BOYS_OK;
+}
+
 // The occupancy query is cached per (kernel, shared-memory size): it is a
 // host-side call that would otherwise sit on every launch's critical path.
 template <typename K>
@@ -726,12 +741,12 @@ static boys_status launch_dense_k(const T* x, int64_t N, T* out, T* expx, int64_
   const bool soa_bulk = !AOS && soa_tma() && (N * (int64_t)sizeof(T)) % 16 == 0 &&
                         (reinterpret_cast<uintptr_t>(out) % 16) == 0;
   size_t smem = (AOS || soa_bulk) ? (size_t)NBUF * kThreads * (n + 1) * sizeof(T) : 0;
-  static bool attr = false;   // per instantiation; sized for the largest use
-  if (!attr) {
+  // the dynamic-smem opt-in is per function *per device*: remember each device
+  static std::atomic<uint64_t> attr_mask{0};
+  {
     const int smem_max = (int)((size_t)NBUF * kThreads * (n + 1) * sizeof(T));
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);
-    if (e != cudaSuccess) return cuda_status(e);
-    attr = true;
+    boys_status st = opt_in_smem(k, smem_max, attr_mask);
+    if (st != BOYS_OK) return st;
   }
   int64_t ntiles = (N + kThreads - 1) / kThreads;
   bool bulk_ok = (reinterpret_cast<uintptr_t>(out) % 16) == 0;
@@ -814,15 +829,6 @@ static boys_status dispatch_split(int nn, int nbar, const void* x, int64_t N, vo
   }
 }
 
-template <typename K>
-static boys_status set_smem(K k, size_t smem, bool& done) {
-  if (done) return BOYS_OK;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return cuda_status(e);
-  done = true;
-  return BOYS_OK;
-}
-
 template <typename T>
 static boys_status launch_ragged(const void* x, const uint8_t* nm, const int64_t* off, int64_t N,
                                  void* out, int64_t* dom, cudaStream_t s) {
@@ -833,8 +839,8 @@ static boys_status launch_ragged(const void* x, const uint8_t* nm, const int64_t
   constexpr int NB = Tab<T>::MAX_ORDER < kRaggedFastOrders ? Tab<T>::MAX_ORDER : kRaggedFastOrders;
   auto k = ragged_kernel<T, NB>;
   const size_t smem = sizeof(RaggedSmem<T, NB>);
-  static bool done = false;
-  boys_status st = set_smem(k, smem, done);
+  static std::atomic<uint64_t> attr_mask{0};
+  boys_status st = opt_in_smem(k, (int)smem, attr_mask);
   if (st != BOYS_OK) return st;
   const int64_t nch = (N + 31) / 32;
   k<<<blocks_for(k, smem, (nch + 7) / 8), kThreads, smem, s>>>((const T*)x, nm, off, N, (T*)out, dom);
