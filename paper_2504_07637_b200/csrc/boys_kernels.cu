@@ -129,103 +129,6 @@ __device__ __forceinline__ void eval_point(T x_in, bool ok, T (&Fv)[n + 1], T& t
   t_out = eval_point_stream<T, n>(x_in, ok, [&](int m, T v) { Fv[m] = v; });
 }
 
-// P independent points per thread, evaluated stage by stage so the compiler
-// can interleave their dependent FP64 chains (ILP for the FP64-bound small
-// orders).  Per point: the same operation sequence as eval_point_stream.
-template <typename T, int n, int P, typename Put>
-__device__ __forceinline__ void eval_points_stream(const T (&xin)[P], const bool (&okin)[P],
-                                                   T (&tout)[P], Put&& put) {
-  using A = Ar<T>;
-  const BoysRow<T>& R = Tab<T>::row(n);
-  const T bad = A::nan();
-  T x[P], t[P], y[P], cur[P], tx[P];
-  bool below = false, up = false;
-#pragma unroll
-  for (int j = 0; j < P; ++j) {
-    x[j] = okin[j] ? xin[j] : T(0);
-    t[j] = exp_neg_clamped(x[j]);
-    below = below || (okin[j] && x[j] < R.z);
-    y[j] = x[j];
-  }
-  if (__any_sync(kFull, below)) {
-    T Q[P];
-#pragma unroll
-    for (int j = 0; j < P; ++j) Q[j] = qtilde<T, n>(x[j], R);
-#pragma unroll
-    for (int j = 0; j < P; ++j) {
-      T sq = A::sqrt(Q[j]);
-      T s = n == 0 ? sq : A::mul(powi<T, (n == 0 ? 1 : n)>(Q[j]), sq);
-      T yq = A::fma(s, t[j], x[j]);
-      y[j] = x[j] < R.z ? yq : x[j];
-    }
-  }
-#pragma unroll
-  for (int j = 0; j < P; ++j) {
-    T r = A::rcp(y[j]);
-    T sr = A::sqrt(r);
-    cur[j] = n == 0 ? A::mul(R.c, sr) : A::mul(A::mul(R.c, powi<T, (n == 0 ? 1 : n)>(r)), sr);
-    put(j, n, okin[j] ? cur[j] : bad);
-    tx[j] = A::add(x[j], x[j]);
-    up = up || (okin[j] && x[j] > R.x_up);
-  }
-#pragma unroll
-  for (int m = n - 1; m >= 0; --m) {
-#pragma unroll
-    for (int j = 0; j < P; ++j) {
-      cur[j] = A::mul(A::fma(tx[j], cur[j], t[j]), rinv<T>(m));
-      put(j, m, okin[j] ? cur[j] : bad);
-    }
-  }
-  if (__any_sync(kFull, up)) {
-#pragma unroll
-    for (int j = 0; j < P; ++j) {
-      const bool upj = okin[j] && x[j] > R.x_up;
-      T rx = A::rcp(x[j]);
-      T f = up_first(x[j]);
-      if (upj) put(j, 0, f);
-#pragma unroll
-      for (int m = 0; m < n; ++m) {
-        f = up_next(f, m, rx);
-        if (upj) put(j, m + 1, f);
-      }
-    }
-  }
-#pragma unroll
-  for (int j = 0; j < P; ++j) tout[j] = okin[j] ? t[j] : bad;
-}
-
-// SoA dense kernel with P points per thread (tile = P x 256 points).
-template <typename T, int n, int P>
-__global__ void __launch_bounds__(kThreads, (P == 1 ? 8 : 5))
-dense_soa_multi_kernel(const T* __restrict__ X, int64_t N, T* __restrict__ out,
-                       T* __restrict__ expx, int64_t* __restrict__ dom, int64_t index_base) {
-  constexpr int TILE = kThreads * P;
-  const int tid = threadIdx.x;
-  const int64_t ntiles = (N + TILE - 1) / TILE;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t i0 = tile * TILE + tid;
-    T x[P], t[P];
-    bool ok[P], in[P];
-#pragma unroll
-    for (int j = 0; j < P; ++j) {
-      const int64_t i = i0 + j * kThreads;
-      in[j] = i < N;
-      x[j] = in[j] ? ldg_nc(X + i) : T(0);
-      ok[j] = valid_x(x[j]);
-      if (in[j] && !ok[j]) flag_domain(dom, index_base + i);
-      ok[j] = ok[j] || !in[j];
-    }
-    eval_points_stream<T, n, P>(x, ok, t, [&](int j, int m, T v) {
-      if (in[j]) __stcs(out + (int64_t)m * N + i0 + j * kThreads, v);
-    });
-    if (expx) {
-#pragma unroll
-      for (int j = 0; j < P; ++j)
-        if (in[j]) __stcs(expx + i0 + j * kThreads, t[j]);
-    }
-  }
-}
-
 // ---------------------------------------------------------------------------
 // dense kernel
 // ---------------------------------------------------------------------------
@@ -817,10 +720,6 @@ static int soa_tma() {   // BOYS_SOA_TMA=1: SoA rows leave as bulk copies
   static int v = env_int("BOYS_SOA_TMA", 0);
   return v;
 }
-static int soa_ppt() {   // BOYS_SOA_PPT: points per thread for n <= 1 SoA (1 or 2)
-  static int v = env_int("BOYS_SOA_PPT", 1) == 2 ? 2 : 1;
-  return v;
-}
 static int grid_tiles() {
   static int v = env_int("BOYS_GRID_TILES", 0);
   return v;
@@ -868,13 +767,6 @@ static boys_status launch_dense_t(const T* x, int64_t N, T* out, T* expx, int64_
     if (soa_tma()) return launch_dense_k<T, n, false, (fits2 ? 2 : 1), 4>(x, N, out, expx, dom, base, s);
     if constexpr (n <= 1) {          // small orders: register budget for 6 or 8 blocks/SM
       if (soa_small_minb() == 6) return launch_dense_k<T, n, false, 1, 6>(x, N, out, expx, dom, base, s);
-      if (soa_ppt() == 2) {          // two points per thread (ILP for the FP64-bound case)
-        auto k = dense_soa_multi_kernel<T, n, 2>;
-        const int64_t ntiles = (N + 2 * kThreads - 1) / (2 * kThreads);
-        k<<<blocks_for(k, 0, ntiles), kThreads, 0, s>>>(x, N, out, expx, dom, base);
-        g_launches.fetch_add(1, std::memory_order_relaxed);
-        return cuda_status(cudaGetLastError());
-      }
     }
     return launch_dense_k<T, n, false, 1, (n <= 1 ? 8 : BOYS_SOA_MINB)>(x, N, out, expx, dom, base, s);
   } else {
