@@ -282,19 +282,19 @@ __device__ __forceinline__ T y_below_rt(T x, T t, int n, const Rows& rows) {
   return A::fma(s, t, x);
 }
 
-// b^n for n < 2^bits (bits: warp-uniform bound); same products as powi<T,n>.
+// b^n for n < 2^bits (bits: warp-uniform bound); same products as powi<T,n>:
+// starting from 1.0 and multiplying by (bit ? b^(2^j) : 1.0) is exact for the
+// unset bits (x * 1.0 == x) and 1.0 * b^(2^j0) == b^(2^j0) for the first set
+// bit, so the rounded product sequence is identical -- with one select per
+// step instead of a select over a conditional product.
 template <typename T>
 __device__ __forceinline__ T powi_rt_bounded(T b, int n, int bits) {
   using A = Ar<T>;
-  T r = b, p = b;
-  bool have = false;
+  T r = T(1), p = b;
 #pragma unroll
   for (int j = 0; j < 6; ++j) {
     if (j >= bits) break;
-    bool bit = (n >> j) & 1;
-    T rr = have ? A::mul(r, p) : p;
-    r = bit ? rr : r;
-    have = have || bit;
+    r = A::mul(r, ((n >> j) & 1) ? p : T(1));
     p = A::mul(p, p);      // unused past the top bit of n: no effect on r
   }
   return r;
