@@ -520,15 +520,36 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
       T cur = n == 0 ? A::mul(cn, sr) : A::mul(A::mul(cn, powi_rt_bounded(r, n, bits)), sr);
       if (wr) dst[n] = cur;
       const T tx = A::add(xs, xs);
-#pragma unroll
-      for (int m = NB - 1; m >= 0; --m) {
-        if (m < wmax) {                            // warp-uniform
-          const T nx = A::mul(A::fma(tx, cur, t), rinv<T>(m));
-          const bool on = m < n;
-          pmov(on, cur, nx);                       // predicated, branch-free
-          psts(on && wr, dst + m, cur);
-        }
+      // recursion steps m = wmax-1 .. 0: enter the unrolled chain once through
+      // a jump table (wmax is warp-uniform) instead of testing every step
+#define BOYS_STEP(M)                                                     \
+  if ((M) < NB) {                                                         \
+    const T nx = A::mul(A::fma(tx, cur, t), rinv<T>((M) < NB ? (M) : 0)); \
+    const bool on = (M) < n;                                              \
+    pmov(on, cur, nx);                                                    \
+    psts(on && wr, dst + (M), cur);                                       \
+  }
+      switch (wmax) {
+        case 16: BOYS_STEP(15) [[fallthrough]];
+        case 15: BOYS_STEP(14) [[fallthrough]];
+        case 14: BOYS_STEP(13) [[fallthrough]];
+        case 13: BOYS_STEP(12) [[fallthrough]];
+        case 12: BOYS_STEP(11) [[fallthrough]];
+        case 11: BOYS_STEP(10) [[fallthrough]];
+        case 10: BOYS_STEP(9) [[fallthrough]];
+        case 9: BOYS_STEP(8) [[fallthrough]];
+        case 8: BOYS_STEP(7) [[fallthrough]];
+        case 7: BOYS_STEP(6) [[fallthrough]];
+        case 6: BOYS_STEP(5) [[fallthrough]];
+        case 5: BOYS_STEP(4) [[fallthrough]];
+        case 4: BOYS_STEP(3) [[fallthrough]];
+        case 3: BOYS_STEP(2) [[fallthrough]];
+        case 2: BOYS_STEP(1) [[fallthrough]];
+        case 1: BOYS_STEP(0) [[fallthrough]];
+        default: break;
       }
+#undef BOYS_STEP
+      static_assert(NB <= 16, "extend the recursion jump table");
       const bool up = wr && ok && xs > rows(n).x_up;
       if (__any_sync(kFull, up)) {
         const T rx = A::rcp(xs);
