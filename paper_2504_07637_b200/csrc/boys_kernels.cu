@@ -314,7 +314,7 @@ __device__ __forceinline__ void tail_rt(T x, T y, T t, int n, bool ok, int wmax,
   T r = A::rcp(y);
   T sr = A::sqrt(r);
   const T c = rows(n).c;
-  T cur = n == 0 ? A::mul(c, sr) : A::mul(A::mul(c, powi_rt_bounded(r, n, bits)), sr);
+  T cur = A::mul(A::mul(c, powi_rt_bounded(r, n, bits)), sr);   // n = 0: exact, see above
   put(n, ok ? cur : bad, true);
   T tx = A::add(x, x);
 #pragma unroll
@@ -517,7 +517,8 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
       const T r = A::rcp(xs);
       const T sr = A::sqrt(r);
       const T cn = rows(n).c;
-      T cur = n == 0 ? A::mul(cn, sr) : A::mul(A::mul(cn, powi_rt_bounded(r, n, bits)), sr);
+      // n = 0: powi gives exactly 1.0 and (c * 1.0) * sr == c * sr, so no select
+      T cur = A::mul(A::mul(cn, powi_rt_bounded(r, n, bits)), sr);
       if (wr) dst[n] = cur;
       const T tx = A::add(xs, xs);
       // recursion steps m = wmax-1 .. 0: enter the unrolled chain once through
