@@ -98,16 +98,19 @@ __device__ __forceinline__ T eval_point_stream(T x_in, bool ok, Put&& put) {
   using A = Ar<T>;
   const BoysRow<T>& R = Tab<T>::row(n);
   const T bad = A::nan();
-  T x = ok ? x_in : T(0);
+  // invalid lanes carry x = NaN: every IEEE step then yields NaN on its own
+  // (t = 0, y = r = F = NaN, the recursion stays NaN, the ladder test is
+  // false) -- no per-value select; valid lanes are untouched
+  T x = ok ? x_in : bad;
   T t = exp_neg_clamped(x);
   bool any_below = __any_sync(kFull, ok && x < R.z);
   T cur = seed<T, n>(x, t, any_below);
-  put(n, ok ? cur : bad);
+  put(n, cur);
   T tx = A::add(x, x);
 #pragma unroll
   for (int m = n - 1; m >= 0; --m) {
     cur = A::mul(A::fma(tx, cur, t), rinv<T>(m));
-    put(m, ok ? cur : bad);
+    put(m, cur);
   }
   bool up = ok && x > R.x_up;
   if (__any_sync(kFull, up)) {
