@@ -591,6 +591,227 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
 }
 
 // ---------------------------------------------------------------------------
+// ragged kernel, block windows (v9): 1024 consecutive elements per window.
+//   P0  load + classify: bucket = order n for elements past their cut-off,
+//       kDeferB for elements below it (Q~ needed), skip for padding;
+//       histogram with warp-aggregated shared atomics (rank within bucket)
+//   P1  scan (warp 0); tasks of <= 32 elements never straddling a bucket
+//   P2  scatter element slots into bucket order
+//   P3  warps take tasks: one compile-time-order tail per task (switch jump
+//       table, no per-lane divergence); the below-cut-off bucket runs the
+//       run-time-order path; values staged at their output offsets
+//   P4  the window's contiguous output range leaves as one bulk copy
+// Windows holding an order above NB, or whose output exceeds the staging
+// capacity, are evaluated per element with direct writes.
+// Values are bit-identical to boys_eval_dense at each element's order.
+// ---------------------------------------------------------------------------
+constexpr int kWin = 1024;                       // elements per window
+constexpr int kWinPer = kWin / kThreads;         // elements per thread in P0
+
+template <typename T, int NB>
+struct RaggedWinSmem {
+  static constexpr int kDeferB = NB + 1, kSkipB = NB + 2, kBuckets = NB + 3;
+  static constexpr int CAP = kWin * 6;           // staged values (ERI-like mean: ~4.1 per element)
+  static constexpr int MAXTASKS = kWin / 32 + kBuckets;
+  SmemTable<T, NB + 1> st;
+  alignas(16) T stage[CAP + 16 / sizeof(T)];
+  T ex[kWin];
+  int eloc[kWin];
+  unsigned char en[kWin];
+  short perm[kWin];
+  int hist[kBuckets];
+  int tstart[MAXTASKS];
+  unsigned char tbucket[MAXTASKS], tcount[MAXTASKS];
+  int ntasks, any_hi;
+};
+
+// compile-time-order tail of a past-cut-off element (y = x) into dst[0..n]
+template <typename T, int n>
+__device__ __forceinline__ void win_tail(T x, bool on, T* dst) {
+  using A = Ar<T>;
+  const BoysRow<T>& R = Tab<T>::row(n);
+  const T t = exp_neg_clamped(x);
+  const T r = A::rcp(x);
+  const T sr = A::sqrt(r);
+  T cur = n == 0 ? A::mul(R.c, sr) : A::mul(A::mul(R.c, powi<T, (n == 0 ? 1 : n)>(r)), sr);
+  if (on) dst[n] = cur;
+  const T tx = A::add(x, x);
+#pragma unroll
+  for (int m = n - 1; m >= 0; --m) {
+    cur = A::mul(A::fma(tx, cur, t), rinv<T>(m));
+    if (on) dst[m] = cur;
+  }
+  const bool up = on && x > R.x_up;
+  if (__any_sync(kFull, up)) {
+    const T rx = A::rcp(x);
+    T f = up_first(x);
+    if (up) dst[0] = f;
+#pragma unroll
+    for (int m = 0; m < n; ++m) {
+      f = up_next(f, m, rx);
+      if (up) dst[m + 1] = f;
+    }
+  }
+}
+
+template <typename T, int NB, int n = 0>
+__device__ __forceinline__ void win_dispatch(int b, T x, bool on, T* dst) {
+  if constexpr (n <= NB) {
+    if (b == n) win_tail<T, n>(x, on, dst);
+    else win_dispatch<T, NB, n + 1>(b, x, on, dst);
+  }
+}
+
+template <typename T, int NB>
+__global__ void __launch_bounds__(kThreads, 2)
+ragged_win_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
+                  const int64_t* __restrict__ OFF, int64_t N, T* __restrict__ out,
+                  int64_t* __restrict__ dom) {
+  using A = Ar<T>;
+  using SM = RaggedWinSmem<T, NB>;
+  constexpr int Q = 16 / sizeof(T), MAXN = Tab<T>::MAX_ORDER;
+  constexpr int kDeferB = SM::kDeferB, kSkipB = SM::kSkipB, kBuckets = SM::kBuckets;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  SM& S = *reinterpret_cast<SM*>(smem_raw);
+  stage_table(S.st);
+  const SmemRows<T> rows{S.st.row};
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  const int64_t nwin = (N + kWin - 1) / kWin;
+  for (int64_t w = blockIdx.x; w < nwin; w += gridDim.x) {
+    const int64_t w0 = w * kWin;
+    const int64_t wl = (w0 + kWin < N) ? w0 + kWin : N;
+    const int64_t base = __ldg(OFF + w0);
+    const int64_t cnt = __ldg(OFF + wl) - base;
+    if (tid < kBuckets) S.hist[tid] = 0;
+    if (tid == 0) S.any_hi = 0;
+    __syncthreads();                                         // (0) previous window done
+    // ---- P0: load, classify, rank within bucket --------------------------
+    int rank[kWinPer], key[kWinPer];
+    bool hi = false;
+#pragma unroll
+    for (int k = 0; k < kWinPer; ++k) {
+      const int slot = k * kThreads + tid;                   // coalesced
+      const int64_t i = w0 + slot;
+      const bool in = i < N;
+      const T x = in ? ldg_nc(X + i) : T(0);
+      const int n = in ? (int)NM[i] : 0;
+      const bool xok = valid_x(x);
+      if (in && !(xok && n <= MAXN)) flag_domain(dom, i);
+      hi = hi || (in && n > NB);
+      const int nn = n <= NB ? n : 0;
+      const T xs = (in && xok) ? x : A::nan();
+      int b = kSkipB;
+      if (in && n <= NB) b = (xok && xs < rows(nn).z) ? kDeferB : nn;
+      S.ex[slot] = xs;
+      S.en[slot] = (unsigned char)nn;
+      S.eloc[slot] = in ? (int)(__ldg(OFF + i) - base) + (int)(base & (Q - 1)) : 0;
+      const unsigned peers = __match_any_sync(kFull, b);
+      const int leader = __ffs(peers) - 1;
+      int b0 = 0;
+      if (lane == leader) b0 = atomicAdd(&S.hist[b], __popc(peers));
+      rank[k] = __shfl_sync(kFull, b0, leader) + __popc(peers & lt);
+      key[k] = b;
+    }
+    if (hi) S.any_hi = 1;
+    if (tid == 0) bulk_wait_read<0>();                       // staging free again
+    __syncthreads();                                         // (1)
+    const bool per_elem = S.any_hi || cnt + Q > SM::CAP;
+    if (per_elem) {
+      // an order above NB or an oversized window: per-element direct writes
+#pragma unroll
+      for (int k = 0; k < kWinPer; ++k) {
+        const int slot = k * kThreads + tid;
+        const int64_t i = w0 + slot;
+        const bool in = i < N;
+        const T x = in ? ldg_nc(X + i) : T(0);
+        const int n = in ? (int)NM[i] : 0;
+        const int64_t goff = in ? __ldg(OFF + i) : 0;
+        if (in && n > MAXN) {
+          for (int m = 0; m <= n; ++m) out[goff + m] = A::nan();
+        }
+        const bool okl = in && valid_x(x) && n <= MAXN;
+        T* dst = out + goff;
+        const bool wr = in && n <= MAXN;
+        eval_point_rt<T, MAXN>(x, okl, okl ? n : 0, ConstRows<T>{},
+                               [&](int m, T v) { if (wr) dst[m] = v; });
+      }
+      continue;
+    }
+    // ---- P1: scan + task list (warp 0) ------------------------------------
+    if (warp == 0) {
+      const int h = lane < kBuckets ? S.hist[lane] : 0;
+      int v = h;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int o = __shfl_up_sync(kFull, v, d);
+        if (lane >= d) v += o;
+      }
+      const int start = v - h;
+      const int nt = (lane < kSkipB) ? (h + 31) / 32 : 0;   // skip bucket has no tasks
+      int tv = nt;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int o = __shfl_up_sync(kFull, tv, d);
+        if (lane >= d) tv += o;
+      }
+      const int t0 = tv - nt;
+      for (int j = 0; j < nt; ++j) {
+        S.tstart[t0 + j] = start + 32 * j;
+        S.tbucket[t0 + j] = (unsigned char)lane;
+        S.tcount[t0 + j] = (unsigned char)min(32, h - 32 * j);
+      }
+      if (lane == 31) S.ntasks = tv;
+      if (lane < kBuckets) S.hist[lane] = start;
+    }
+    __syncthreads();                                         // (2)
+    // ---- P2: scatter slots into bucket order --------------------------------
+#pragma unroll
+    for (int k = 0; k < kWinPer; ++k)
+      if (key[k] != kSkipB) S.perm[S.hist[key[k]] + rank[k]] = (short)(k * kThreads + tid);
+    __syncthreads();                                         // (3)
+    // ---- P3: tasks ------------------------------------------------------------
+    const int ntasks = S.ntasks;
+    for (int tk = warp; tk < ntasks; tk += kThreads / 32) {
+      const int b = S.tbucket[tk];
+      const bool has = lane < S.tcount[tk];
+      const int e = has ? S.perm[S.tstart[tk] + lane] : 0;
+      const T x = has ? S.ex[e] : T(0);
+      T* dst = S.stage + (has ? S.eloc[e] : 0);
+      if (b == kDeferB) {
+        const int n = has ? (int)S.en[e] : 0;
+        const T xe = has ? x : T(0);
+        const T t = exp_neg_clamped(xe);
+        const T y = has ? y_below_rt(xe, t, n, rows) : xe;
+        const int wmax = __reduce_max_sync(kFull, (unsigned)n);
+        T* sink = S.stage + SM::CAP + (lane & (Q - 1));     // beyond the staged range
+        tail_rt<T, NB>(xe, y, t, n, has, wmax, rows,
+                       [&](int m, T v, bool on) { *((has && on) ? dst + m : sink) = v; });
+      } else {
+        win_dispatch<T, NB>(b, has ? x : T(1), has, dst);
+      }
+    }
+    __syncthreads();                                         // (4) staging complete
+    // ---- P4: one bulk copy of the window's output range -----------------------
+    if (warp == 0) {
+      const int shift = (int)(base & (Q - 1));
+      const int ncnt = (int)cnt;
+      const int head = ((Q - shift) & (Q - 1)) < ncnt ? ((Q - shift) & (Q - 1)) : ncnt;
+      const int body = ((ncnt - head) / Q) * Q;
+      const int tail0 = head + body;
+      if (lane < head) __stcs(out + base + lane, S.stage[shift + lane]);
+      if (lane < ncnt - tail0) __stcs(out + base + tail0 + lane, S.stage[shift + tail0 + lane]);
+      if (body > 0) {
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) bulk_store(out + base + head, S.stage + shift + head, body * sizeof(T));
+      }
+    }
+  }
+  if (tid == 0) bulk_wait_all();
+}
+
+// ---------------------------------------------------------------------------
 // split kernel (eval_with_split): F_m for m <= nbar equals a
 // dense order-nbar evaluation, F_m for m > nbar a dense order-n evaluation.
 // ---------------------------------------------------------------------------
@@ -854,21 +1075,35 @@ static boys_status dispatch_split(int nn, int nbar, const void* x, int64_t N, vo
   }
 }
 
+static int ragged_win() {   // BOYS_RAGGED_WIN=0 selects the warp-chunk kernel (v7)
+  static int v = env_int("BOYS_RAGGED_WIN", 1);
+  return v;
+}
+
 template <typename T>
 static boys_status launch_ragged(const void* x, const uint8_t* nm, const int64_t* off, int64_t N,
                                  void* out, int64_t* dom, cudaStream_t s) {
-  // fast-path order bound (staging per warp = 32 x (NB+1) values); higher
-  // orders, up to the table maximum, take the in-kernel fallback path.
-  // (Order-sorted super-chunks of 64/128 elements were measured slower on
-  // B200: 2.90 / 3.79 ms vs 2.42 ms for cfg4 -- more registers and smem.)
+  // fast-path order bound; higher orders, up to the table maximum, take the
+  // in-kernel per-element fallback path
   constexpr int NB = Tab<T>::MAX_ORDER < kRaggedFastOrders ? Tab<T>::MAX_ORDER : kRaggedFastOrders;
-  auto k = ragged_kernel<T, NB>;
-  const size_t smem = sizeof(RaggedSmem<T, NB>);
-  static std::atomic<uint64_t> attr_mask{0};
-  boys_status st = opt_in_smem(k, (int)smem, attr_mask);
-  if (st != BOYS_OK) return st;
-  const int64_t nch = (N + 31) / 32;
-  k<<<blocks_for(k, smem, (nch + 7) / 8), kThreads, smem, s>>>((const T*)x, nm, off, N, (T*)out, dom);
+  if (ragged_win()) {
+    auto k = ragged_win_kernel<T, NB>;
+    const size_t smem = sizeof(RaggedWinSmem<T, NB>);
+    static std::atomic<uint64_t> attr_mask{0};
+    boys_status st = opt_in_smem(k, (int)smem, attr_mask);
+    if (st != BOYS_OK) return st;
+    const int64_t nwin = (N + kWin - 1) / kWin;
+    k<<<blocks_for(k, smem, nwin), kThreads, smem, s>>>((const T*)x, nm, off, N, (T*)out, dom);
+  } else {
+    // (order-sorted warp super-chunks were measured slower: 2.90 / 3.79 ms vs 2.42)
+    auto k = ragged_kernel<T, NB>;
+    const size_t smem = sizeof(RaggedSmem<T, NB>);
+    static std::atomic<uint64_t> attr_mask{0};
+    boys_status st = opt_in_smem(k, (int)smem, attr_mask);
+    if (st != BOYS_OK) return st;
+    const int64_t nch = (N + 31) / 32;
+    k<<<blocks_for(k, smem, (nch + 7) / 8), kThreads, smem, s>>>((const T*)x, nm, off, N, (T*)out, dom);
+  }
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cuda_status(cudaGetLastError());
 }
