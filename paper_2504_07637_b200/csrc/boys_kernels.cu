@@ -663,7 +663,7 @@ __device__ __forceinline__ void win_dispatch(int b, T x, bool on, T* dst) {
 }
 
 template <typename T, int NB>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, 3)
 ragged_win_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
                   const int64_t* __restrict__ OFF, int64_t N, T* __restrict__ out,
                   int64_t* __restrict__ dom) {
@@ -678,15 +678,35 @@ ragged_win_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned lt = (1u << lane) - 1u;
   const int64_t nwin = (N + kWin - 1) / kWin;
+  // software pipeline: the next window's inputs are loaded into registers
+  // while the current window runs P1..P4
+  T px[kWinPer];
+  int pn[kWinPer];
+  int64_t poff[kWinPer], pbase = 0, plast = 0;
+  auto load = [&](int64_t ww) {
+    if (ww >= nwin) return;
+    const int64_t a0 = ww * kWin;
+    const int64_t al = (a0 + kWin < N) ? a0 + kWin : N;
+    pbase = __ldg(OFF + a0);
+    plast = __ldg(OFF + al);
+#pragma unroll
+    for (int k = 0; k < kWinPer; ++k) {
+      const int64_t i = a0 + k * kThreads + tid;
+      const bool in = i < N;
+      px[k] = in ? ldg_nc(X + i) : T(0);
+      pn[k] = in ? (int)NM[i] : 0;
+      poff[k] = in ? __ldg(OFF + i) : 0;
+    }
+  };
+  load(blockIdx.x);
   for (int64_t w = blockIdx.x; w < nwin; w += gridDim.x) {
     const int64_t w0 = w * kWin;
-    const int64_t wl = (w0 + kWin < N) ? w0 + kWin : N;
-    const int64_t base = __ldg(OFF + w0);
-    const int64_t cnt = __ldg(OFF + wl) - base;
+    const int64_t base = pbase;
+    const int64_t cnt = plast - pbase;
     if (tid < kBuckets) S.hist[tid] = 0;
     if (tid == 0) S.any_hi = 0;
     __syncthreads();                                         // (0) previous window done
-    // ---- P0: load, classify, rank within bucket --------------------------
+    // ---- P0: classify, rank within bucket ---------------------------------
     int rank[kWinPer], key[kWinPer];
     bool hi = false;
 #pragma unroll
@@ -694,8 +714,8 @@ ragged_win_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
       const int slot = k * kThreads + tid;                   // coalesced
       const int64_t i = w0 + slot;
       const bool in = i < N;
-      const T x = in ? ldg_nc(X + i) : T(0);
-      const int n = in ? (int)NM[i] : 0;
+      const T x = px[k];
+      const int n = pn[k];
       const bool xok = valid_x(x);
       if (in && !(xok && n <= MAXN)) flag_domain(dom, i);
       hi = hi || (in && n > NB);
@@ -705,7 +725,7 @@ ragged_win_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
       if (in && n <= NB) b = (xok && xs < rows(nn).z) ? kDeferB : nn;
       S.ex[slot] = xs;
       S.en[slot] = (unsigned char)nn;
-      S.eloc[slot] = in ? (int)(__ldg(OFF + i) - base) + (int)(base & (Q - 1)) : 0;
+      S.eloc[slot] = in ? (int)(poff[k] - base) + (int)(base & (Q - 1)) : 0;
       const unsigned peers = __match_any_sync(kFull, b);
       const int leader = __ffs(peers) - 1;
       int b0 = 0;
@@ -714,6 +734,7 @@ ragged_win_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
       key[k] = b;
     }
     if (hi) S.any_hi = 1;
+    load(w + gridDim.x);                                     // prefetch the next window
     if (tid == 0) bulk_wait_read<0>();                       // staging free again
     __syncthreads();                                         // (1)
     const bool per_elem = S.any_hi || cnt + Q > SM::CAP;
