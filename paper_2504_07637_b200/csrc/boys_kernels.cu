@@ -622,7 +622,7 @@ struct RaggedWinSmem {
   int hist[kBuckets];
   int tstart[MAXTASKS];
   unsigned char tbucket[MAXTASKS], tcount[MAXTASKS];
-  int ntasks, any_hi;
+  int ntasks, any_hi, next_task;
 };
 
 // compile-time-order tail of a past-cut-off element (y = x) into dst[0..n]
@@ -704,7 +704,7 @@ ragged_win_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
     const int64_t base = pbase;
     const int64_t cnt = plast - pbase;
     if (tid < kBuckets) S.hist[tid] = 0;
-    if (tid == 0) S.any_hi = 0;
+    if (tid == 0) { S.any_hi = 0; S.next_task = 0; }
     __syncthreads();                                         // (0) previous window done
     // ---- P0: classify, rank within bucket ---------------------------------
     int rank[kWinPer], key[kWinPer];
@@ -792,8 +792,16 @@ ragged_win_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
       if (key[k] != kSkipB) S.perm[S.hist[key[k]] + rank[k]] = (short)(k * kThreads + tid);
     __syncthreads();                                         // (3)
     // ---- P3: tasks ------------------------------------------------------------
+    // tasks are taken dynamically, most expensive first (the task list is
+    // built in ascending bucket order: below-cut-off bucket last, so walking
+    // it backwards is longest-processing-time-first)
     const int ntasks = S.ntasks;
-    for (int tk = warp; tk < ntasks; tk += kThreads / 32) {
+    for (;;) {
+      int tk = 0;
+      if (lane == 0) tk = atomicAdd(&S.next_task, 1);
+      tk = __shfl_sync(kFull, tk, 0);
+      if (tk >= ntasks) break;
+      tk = ntasks - 1 - tk;
       const int b = S.tbucket[tk];
       const bool has = lane < S.tcount[tk];
       const int e = has ? S.perm[S.tstart[tk] + lane] : 0;
