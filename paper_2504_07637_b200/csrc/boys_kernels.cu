@@ -605,13 +605,13 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
 // capacity, are evaluated per element with direct writes.
 // Values are bit-identical to boys_eval_dense at each element's order.
 // ---------------------------------------------------------------------------
-constexpr int kWin = 1024;                       // elements per window
+constexpr int kWin = 768;                        // elements per window
 constexpr int kWinPer = kWin / kThreads;         // elements per thread in P0
 
 template <typename T, int NB>
 struct RaggedWinSmem {
   static constexpr int kDeferB = NB + 1, kSkipB = NB + 2, kBuckets = NB + 3;
-  static constexpr int CAP = kWin * 6;           // staged values (ERI-like mean: ~4.1 per element)
+  static constexpr int CAP = kWin * 11 / 2;      // staged values (ERI-like mean: ~4.1 per element)
   static constexpr int MAXTASKS = kWin / 32 + kBuckets;
   SmemTable<T, NB + 1> st;
   alignas(16) T stage[CAP + 16 / sizeof(T)];
@@ -663,7 +663,7 @@ __device__ __forceinline__ void win_dispatch(int b, T x, bool on, T* dst) {
 }
 
 template <typename T, int NB>
-__global__ void __launch_bounds__(kThreads, 3)
+__global__ void __launch_bounds__(kThreads, 4)
 ragged_win_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
                   const int64_t* __restrict__ OFF, int64_t N, T* __restrict__ out,
                   int64_t* __restrict__ dom) {
@@ -792,16 +792,8 @@ ragged_win_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
       if (key[k] != kSkipB) S.perm[S.hist[key[k]] + rank[k]] = (short)(k * kThreads + tid);
     __syncthreads();                                         // (3)
     // ---- P3: tasks ------------------------------------------------------------
-    // tasks are taken dynamically, most expensive first (the task list is
-    // built in ascending bucket order: below-cut-off bucket last, so walking
-    // it backwards is longest-processing-time-first)
     const int ntasks = S.ntasks;
-    for (;;) {
-      int tk = 0;
-      if (lane == 0) tk = atomicAdd(&S.next_task, 1);
-      tk = __shfl_sync(kFull, tk, 0);
-      if (tk >= ntasks) break;
-      tk = ntasks - 1 - tk;
+    for (int tk = warp; tk < ntasks; tk += kThreads / 32) {
       const int b = S.tbucket[tk];
       const bool has = lane < S.tcount[tk];
       const int e = has ? S.perm[S.tstart[tk] + lane] : 0;
