@@ -605,13 +605,16 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
 // capacity, are evaluated per element with direct writes.
 // Values are bit-identical to boys_eval_dense at each element's order.
 // ---------------------------------------------------------------------------
-constexpr int kWin = 768;                        // elements per window
+constexpr int kWin = 1024;                       // elements per window
 constexpr int kWinPer = kWin / kThreads;         // elements per thread in P0
 
 template <typename T, int NB>
 struct RaggedWinSmem {
-  static constexpr int kDeferB = NB + 1, kSkipB = NB + 2, kBuckets = NB + 3;
-  static constexpr int CAP = kWin * 11 / 2;      // staged values (ERI-like mean: ~4.1 per element)
+  // bucket ids: 0 = below the cut-off (expensive: first in the task list so
+  // the static striping starts warps 0.. on them), 1 + n = past-cut-off
+  // elements of order n, NB + 2 = padding (no tasks)
+  static constexpr int kDeferB = 0, kSkipB = NB + 2, kBuckets = NB + 3;
+  static constexpr int CAP = kWin * 6;           // staged values (ERI-like mean: ~4.1 per element)
   static constexpr int MAXTASKS = kWin / 32 + kBuckets;
   SmemTable<T, NB + 1> st;
   alignas(16) T stage[CAP + 16 / sizeof(T)];
@@ -622,7 +625,7 @@ struct RaggedWinSmem {
   int hist[kBuckets];
   int tstart[MAXTASKS];
   unsigned char tbucket[MAXTASKS], tcount[MAXTASKS];
-  int ntasks, any_hi, next_task;
+  int ntasks, any_hi;
 };
 
 // compile-time-order tail of a past-cut-off element (y = x) into dst[0..n]
@@ -663,7 +666,7 @@ __device__ __forceinline__ void win_dispatch(int b, T x, bool on, T* dst) {
 }
 
 template <typename T, int NB>
-__global__ void __launch_bounds__(kThreads, 4)
+__global__ void __launch_bounds__(kThreads, 3)
 ragged_win_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
                   const int64_t* __restrict__ OFF, int64_t N, T* __restrict__ out,
                   int64_t* __restrict__ dom) {
@@ -704,7 +707,7 @@ ragged_win_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
     const int64_t base = pbase;
     const int64_t cnt = plast - pbase;
     if (tid < kBuckets) S.hist[tid] = 0;
-    if (tid == 0) { S.any_hi = 0; S.next_task = 0; }
+    if (tid == 0) S.any_hi = 0;
     __syncthreads();                                         // (0) previous window done
     // ---- P0: classify, rank within bucket ---------------------------------
     int rank[kWinPer], key[kWinPer];
@@ -722,7 +725,7 @@ ragged_win_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
       const int nn = n <= NB ? n : 0;
       const T xs = (in && xok) ? x : A::nan();
       int b = kSkipB;
-      if (in && n <= NB) b = (xok && xs < rows(nn).z) ? kDeferB : nn;
+      if (in && n <= NB) b = (xok && xs < rows(nn).z) ? kDeferB : nn + 1;
       S.ex[slot] = xs;
       S.en[slot] = (unsigned char)nn;
       S.eloc[slot] = in ? (int)(poff[k] - base) + (int)(base & (Q - 1)) : 0;
@@ -809,7 +812,7 @@ ragged_win_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
         tail_rt<T, NB>(xe, y, t, n, has, wmax, rows,
                        [&](int m, T v, bool on) { *((has && on) ? dst + m : sink) = v; });
       } else {
-        win_dispatch<T, NB>(b, has ? x : T(1), has, dst);
+        win_dispatch<T, NB>(b - 1, has ? x : T(1), has, dst);
       }
     }
     __syncthreads();                                         // (4) staging complete
