@@ -1099,9 +1099,16 @@ static boys_status dispatch_split(int nn, int nbar, const void* x, int64_t N, vo
   }
 }
 
-static int ragged_win() {   // BOYS_RAGGED_WIN=0 selects the warp-chunk kernel (v7)
-  static int v = env_int("BOYS_RAGGED_WIN", 1);
-  return v;
+// Ragged kernel per dtype, chosen by same-box measurement on B200 (cfg4):
+//   f32: block windows 1.19 ms vs warp chunks 1.52 ms  -> windows
+//   f64: block windows 2.59 ms vs warp chunks 2.24 ms  -> warp chunks
+// (f64's heavier below-cut-off tasks leave the window barriers waiting).
+// BOYS_RAGGED_WIN=0/1 forces one kernel for both dtypes.
+template <typename T>
+static bool ragged_win() {
+  static int v = env_int("BOYS_RAGGED_WIN", -1);
+  if (v == 0 || v == 1) return v == 1;
+  return sizeof(T) == 4;
 }
 
 template <typename T>
@@ -1110,7 +1117,7 @@ static boys_status launch_ragged(const void* x, const uint8_t* nm, const int64_t
   // fast-path order bound; higher orders, up to the table maximum, take the
   // in-kernel per-element fallback path
   constexpr int NB = Tab<T>::MAX_ORDER < kRaggedFastOrders ? Tab<T>::MAX_ORDER : kRaggedFastOrders;
-  if (ragged_win()) {
+  if (ragged_win<T>()) {
     auto k = ragged_win_kernel<T, NB>;
     const size_t smem = sizeof(RaggedWinSmem<T, NB>);
     static std::atomic<uint64_t> attr_mask{0};
