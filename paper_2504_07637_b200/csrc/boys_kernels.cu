@@ -605,17 +605,17 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
 // capacity, are evaluated per element with direct writes.
 // Values are bit-identical to boys_eval_dense at each element's order.
 // ---------------------------------------------------------------------------
-constexpr int kWin = 1024;                       // elements per window
-constexpr int kWinPer = kWin / kThreads;         // elements per thread in P0
+constexpr int kWinPer = 4;                       // elements per thread per window
 
-template <typename T, int NB>
+template <typename T, int NB, int WT>
 struct RaggedWinSmem {
+  static constexpr int kWin = WT * kWinPer;
   // bucket ids: 0 = below the cut-off (expensive: first in the task list so
   // the static striping starts warps 0.. on them), 1 + n = past-cut-off
   // elements of order n, NB + 2 = padding (no tasks)
   static constexpr int kDeferB = 0, kSkipB = NB + 2, kBuckets = NB + 3;
   static constexpr int CAP = kWin * 6;           // staged values (ERI-like mean: ~4.1 per element)
-  static constexpr int MAXTASKS = kWin / 32 + kBuckets;
+  static constexpr int MAXTASKS = (WT * kWinPer) / 32 + kBuckets;
   SmemTable<T, NB + 1> st;
   alignas(16) T stage[CAP + 16 / sizeof(T)];
   T ex[kWin];
@@ -665,13 +665,14 @@ __device__ __forceinline__ void win_dispatch(int b, T x, bool on, T* dst) {
   }
 }
 
-template <typename T, int NB>
-__global__ void __launch_bounds__(kThreads, 3)
+template <typename T, int NB, int WT>
+__global__ void __launch_bounds__(WT, (WT == 128 ? 6 : WT == 256 ? 3 : 1))
 ragged_win_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
                   const int64_t* __restrict__ OFF, int64_t N, T* __restrict__ out,
                   int64_t* __restrict__ dom) {
   using A = Ar<T>;
-  using SM = RaggedWinSmem<T, NB>;
+  using SM = RaggedWinSmem<T, NB, WT>;
+  constexpr int kWin = SM::kWin;
   constexpr int Q = 16 / sizeof(T), MAXN = Tab<T>::MAX_ORDER;
   constexpr int kDeferB = SM::kDeferB, kSkipB = SM::kSkipB, kBuckets = SM::kBuckets;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -694,7 +695,7 @@ ragged_win_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
     plast = __ldg(OFF + al);
 #pragma unroll
     for (int k = 0; k < kWinPer; ++k) {
-      const int64_t i = a0 + k * kThreads + tid;
+      const int64_t i = a0 + k * WT + tid;
       const bool in = i < N;
       px[k] = in ? ldg_nc(X + i) : T(0);
       pn[k] = in ? (int)NM[i] : 0;
@@ -714,7 +715,7 @@ ragged_win_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
     bool hi = false;
 #pragma unroll
     for (int k = 0; k < kWinPer; ++k) {
-      const int slot = k * kThreads + tid;                   // coalesced
+      const int slot = k * WT + tid;                   // coalesced
       const int64_t i = w0 + slot;
       const bool in = i < N;
       const T x = px[k];
@@ -745,7 +746,7 @@ ragged_win_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
       // an order above NB or an oversized window: per-element direct writes
 #pragma unroll
       for (int k = 0; k < kWinPer; ++k) {
-        const int slot = k * kThreads + tid;
+        const int slot = k * WT + tid;
         const int64_t i = w0 + slot;
         const bool in = i < N;
         const T x = in ? ldg_nc(X + i) : T(0);
@@ -792,11 +793,11 @@ ragged_win_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
     // ---- P2: scatter slots into bucket order --------------------------------
 #pragma unroll
     for (int k = 0; k < kWinPer; ++k)
-      if (key[k] != kSkipB) S.perm[S.hist[key[k]] + rank[k]] = (short)(k * kThreads + tid);
+      if (key[k] != kSkipB) S.perm[S.hist[key[k]] + rank[k]] = (short)(k * WT + tid);
     __syncthreads();                                         // (3)
     // ---- P3: tasks ------------------------------------------------------------
     const int ntasks = S.ntasks;
-    for (int tk = warp; tk < ntasks; tk += kThreads / 32) {
+    for (int tk = warp; tk < ntasks; tk += WT / 32) {
       const int b = S.tbucket[tk];
       const bool has = lane < S.tcount[tk];
       const int e = has ? S.perm[S.tstart[tk] + lane] : 0;
@@ -1111,6 +1112,29 @@ static bool ragged_win() {
   return sizeof(T) == 4;
 }
 
+static int ragged_win_threads() {   // BOYS_RAGGED_WT: window block size (128/256/512)
+  static int v = env_int("BOYS_RAGGED_WT", 256);
+  return v;
+}
+
+template <typename T, int NB, int WT>
+static boys_status launch_win(const void* x, const uint8_t* nm, const int64_t* off, int64_t N,
+                              void* out, int64_t* dom, cudaStream_t s) {
+  auto k = ragged_win_kernel<T, NB, WT>;
+  const size_t smem = sizeof(RaggedWinSmem<T, NB, WT>);
+  static std::atomic<uint64_t> attr_mask{0};
+  boys_status st = opt_in_smem(k, (int)smem, attr_mask);
+  if (st != BOYS_OK) return st;
+  const int64_t win = (int64_t)WT * kWinPer;
+  const int64_t nwin = (N + win - 1) / win;
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, WT, smem);
+  int64_t grid = (int64_t)sm_count() * (occ < 1 ? 1 : occ);
+  if (nwin < grid) grid = nwin;
+  k<<<(int)(grid < 1 ? 1 : grid), WT, smem, s>>>((const T*)x, nm, off, N, (T*)out, dom);
+  return cuda_status(cudaGetLastError());
+}
+
 template <typename T>
 static boys_status launch_ragged(const void* x, const uint8_t* nm, const int64_t* off, int64_t N,
                                  void* out, int64_t* dom, cudaStream_t s) {
@@ -1118,13 +1142,12 @@ static boys_status launch_ragged(const void* x, const uint8_t* nm, const int64_t
   // in-kernel per-element fallback path
   constexpr int NB = Tab<T>::MAX_ORDER < kRaggedFastOrders ? Tab<T>::MAX_ORDER : kRaggedFastOrders;
   if (ragged_win<T>()) {
-    auto k = ragged_win_kernel<T, NB>;
-    const size_t smem = sizeof(RaggedWinSmem<T, NB>);
-    static std::atomic<uint64_t> attr_mask{0};
-    boys_status st = opt_in_smem(k, (int)smem, attr_mask);
+    const int wt = ragged_win_threads();
+    boys_status st = BOYS_OK;
+    if (wt == 128) st = launch_win<T, NB, 128>(x, nm, off, N, out, dom, s);
+    else if (wt == 512) st = launch_win<T, NB, 512>(x, nm, off, N, out, dom, s);
+    else st = launch_win<T, NB, 256>(x, nm, off, N, out, dom, s);
     if (st != BOYS_OK) return st;
-    const int64_t nwin = (N + kWin - 1) / kWin;
-    k<<<blocks_for(k, smem, nwin), kThreads, smem, s>>>((const T*)x, nm, off, N, (T*)out, dom);
   } else {
     // (order-sorted warp super-chunks were measured slower: 2.90 / 3.79 ms vs 2.42)
     auto k = ragged_kernel<T, NB>;
