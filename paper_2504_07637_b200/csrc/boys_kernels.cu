@@ -1112,11 +1112,6 @@ static bool ragged_win() {
   return sizeof(T) == 4;
 }
 
-static int ragged_win_threads() {   // BOYS_RAGGED_WT: window block size (128/256/512)
-  static int v = env_int("BOYS_RAGGED_WT", 256);
-  return v;
-}
-
 template <typename T, int NB, int WT>
 static boys_status launch_win(const void* x, const uint8_t* nm, const int64_t* off, int64_t N,
                               void* out, int64_t* dom, cudaStream_t s) {
@@ -1142,11 +1137,9 @@ static boys_status launch_ragged(const void* x, const uint8_t* nm, const int64_t
   // in-kernel per-element fallback path
   constexpr int NB = Tab<T>::MAX_ORDER < kRaggedFastOrders ? Tab<T>::MAX_ORDER : kRaggedFastOrders;
   if (ragged_win<T>()) {
-    const int wt = ragged_win_threads();
-    boys_status st = BOYS_OK;
-    if (wt == 128) st = launch_win<T, NB, 128>(x, nm, off, N, out, dom, s);
-    else if (wt == 512) st = launch_win<T, NB, 512>(x, nm, off, N, out, dom, s);
-    else st = launch_win<T, NB, 256>(x, nm, off, N, out, dom, s);
+    // 256-thread blocks / 1024-element windows: measured best (f32 cfg4:
+    // 128 -> 1.27 ms, 256 -> 1.19 ms, 512 -> 2.04 ms)
+    boys_status st = launch_win<T, NB, 256>(x, nm, off, N, out, dom, s);
     if (st != BOYS_OK) return st;
   } else {
     // (order-sorted warp super-chunks were measured slower: 2.90 / 3.79 ms vs 2.42)
