@@ -366,7 +366,7 @@ __device__ __forceinline__ void eval_point_rt(T x_in, bool ok, int n, const Rows
 // ---------------------------------------------------------------------------
 // ragged kernel: element i, order n_i, values at out[offsets[i] + m]
 //
-// Warp-autonomous (no block barriers): each warp walks 32-element chunks.
+// Warp-autonomous (no block barriers): each warp walks chunks of 32*EPL elements.
 //   * every lane: e^{-x}; elements past their cut-off (x >= z_{n_i}, ~95% of
 //     ERI-like batches) run the cheap run-time-order tail at once into the
 //     warp's staging slot; the chunk's contiguous output range then leaves
@@ -376,25 +376,36 @@ __device__ __forceinline__ void eval_point_rt(T x_in, bool ok, int n, const Rows
 //     each lane writing its element's n+1 values directly.
 // Values are bit-identical to boys_eval_dense at each element's order.
 // ---------------------------------------------------------------------------
-template <typename T, int NB>
+// EPL elements per lane (chunks of 32*EPL elements): the warp-uniform work of
+// a chunk (ballots, jump-table dispatch, bulk store, constant loads) is shared
+// by EPL elements per lane, whose independent chains also interleave (ILP).
+// Staging holds CAP values; a chunk whose output range exceeds it takes the
+// per-element direct-write path (never for ERI-like order mixes).
+template <int NB, int EPL> struct RaggedCap {
+  static constexpr int value = EPL == 1 ? 32 * (NB + 1) : 32 * EPL * (NB < 11 ? NB + 1 : 12);
+};
+
+template <typename T, int NB, int EPL>
 struct RaggedWarp {
-  alignas(16) T stage[32 * (NB + 1) + 16 / sizeof(T)];
-  T qx[64], qt[64];
-  int64_t qoff[64];
-  unsigned char qn[64];
+  static constexpr int CAP = RaggedCap<NB, EPL>::value;
+  static constexpr int QCAP = 32 * EPL + 32;      // < 32 left after a drain + one chunk
+  alignas(16) T stage[CAP + 16 / sizeof(T)];
+  T qx[QCAP], qt[QCAP];
+  int64_t qoff[QCAP];
+  unsigned char qn[QCAP];
   T scratch[32];
 };
 
-template <typename T, int NB>
+template <typename T, int NB, int EPL>
 struct RaggedSmem {
   SmemTable<T, NB + 1> st;           // rows 0..NB (the fast path's orders)
-  RaggedWarp<T, NB> w[kThreads / 32];
+  RaggedWarp<T, NB, EPL> w[kThreads / 32];
 };
 
 // Evaluate up to 32 queued below-cut-off elements (one per lane), writing
 // straight to global memory.
-template <typename T, int NB>
-__device__ __forceinline__ void ragged_drain(RaggedWarp<T, NB>& W, const SmemRows<T>& st,
+template <typename T, int NB, typename WarpT>
+__device__ __forceinline__ void ragged_drain(WarpT& W, const SmemRows<T>& st,
                                              int& qn, int lane, T* __restrict__ out) {
   // queued elements' slots were written (with stale staging data) by earlier
   // bulk stores of their chunks: those must be complete before we overwrite
@@ -429,109 +440,143 @@ template <> struct Sentinel<float> {
   static __device__ __forceinline__ bool is(float v) { return __float_as_int(v) == 0x7fa0c0de; }
 };
 
-template <typename T, int NB>
+template <typename T, int NB, int EPL>
 __global__ void __launch_bounds__(kThreads)
 ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
               const int64_t* __restrict__ OFF, int64_t N, T* __restrict__ out,
               int64_t* __restrict__ dom) {
   using A = Ar<T>;
+  using WarpT = RaggedWarp<T, NB, EPL>;
+  constexpr int CH = 32 * EPL;                   // elements per chunk
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  RaggedSmem<T, NB>& S = *reinterpret_cast<RaggedSmem<T, NB>*>(smem_raw);
+  RaggedSmem<T, NB, EPL>& S = *reinterpret_cast<RaggedSmem<T, NB, EPL>*>(smem_raw);
   stage_table(S.st);
   __syncthreads();
   const SmemRows<T> rows{S.st.row};
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  RaggedWarp<T, NB>& W = S.w[wid];
-  const int64_t nchunks = (N + 31) / 32;
+  WarpT& W = S.w[wid];
+  const int64_t nchunks = (N + CH - 1) / CH;
   const int64_t wstride = (int64_t)gridDim.x * (kThreads / 32);
   int qn = 0;                                    // warp-uniform queue length
   int64_t c = (int64_t)blockIdx.x * (kThreads / 32) + wid;
   // software pipeline: inputs of chunk c are loaded one iteration ahead
-  T px = T(0);
-  int pn = 0;
-  int64_t poff = 0, pbase = 0, plast_off = 0;
+  T px[EPL];
+  int pn[EPL];
+  int64_t poff[EPL], pbase = 0, plast_off = 0;
   auto load = [&](int64_t cc) {
-    const int64_t j0 = cc * 32, j = j0 + lane;
-    const bool jin = cc < nchunks && j < N;
-    px = jin ? ldg_nc(X + j) : T(0);
-    pn = jin ? (int)NM[j] : 0;
-    poff = jin ? __ldg(OFF + j) : 0;
+    const int64_t j0 = cc * CH;
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) {
+      const int64_t j = j0 + 32 * e + lane;
+      const bool jin = cc < nchunks && j < N;
+      px[e] = jin ? ldg_nc(X + j) : T(0);
+      pn[e] = jin ? (int)NM[j] : 0;
+      poff[e] = jin ? __ldg(OFF + j) : 0;
+    }
     if (cc < nchunks) {
       pbase = __ldg(OFF + j0);
-      plast_off = __ldg(OFF + ((j0 + 32 < N) ? j0 + 32 : N));
+      plast_off = __ldg(OFF + ((j0 + CH < N) ? j0 + CH : N));
     }
   };
   load(c);
   for (; c < nchunks; c += wstride) {
-    const int64_t i0 = c * 32;
-    const int64_t i = i0 + lane;
-    const bool in = i < N;
-    const T x = px;
-    const int n = pn;
-    const int64_t goff = poff, base = pbase, cnt = plast_off - pbase;
+    const int64_t i0 = c * CH;
+    T x[EPL];
+    int n[EPL];
+    int64_t goff[EPL];
+    bool in[EPL];
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) {
+      x[e] = px[e];
+      n[e] = pn[e];
+      goff[e] = poff[e];
+      in[e] = i0 + 32 * e + lane < N;
+    }
+    const int64_t base = pbase, cnt = plast_off - pbase;
     load(c + wstride);
     constexpr int MAXN = Tab<T>::MAX_ORDER;
-    const bool xok = valid_x(x);
-    if (in && !(xok && n <= MAXN)) flag_domain(dom, i);
-    if (__any_sync(kFull, in && n > NB)) {
-      // an order above the fast path's bound: every lane evaluates its own
-      // element from the __constant__ rows and writes it directly (NaN for
-      // orders above the table)
-      if (in && n > MAXN) {
-        for (int m = 0; m <= n; ++m) out[goff + m] = A::nan();
+    bool xok[EPL], slow = cnt > WarpT::CAP;
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) {
+      xok[e] = valid_x(x[e]);
+      if (in[e] && !(xok[e] && n[e] <= MAXN)) flag_domain(dom, i0 + 32 * e + lane);
+      slow = slow || (in[e] && n[e] > NB);
+    }
+    if (__any_sync(kFull, slow)) {
+      // an order above the fast path's bound (or an output range above the
+      // staging capacity): every lane evaluates its own elements from the
+      // __constant__ rows and writes them directly (NaN above the table)
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) {
+        if (in[e] && n[e] > MAXN) {
+          for (int m = 0; m <= n[e]; ++m) out[goff[e] + m] = A::nan();
+        }
+        const bool okl = in[e] && xok[e] && n[e] <= MAXN;
+        T* dst = out + goff[e];
+        const bool wd = in[e] && n[e] <= MAXN;
+        eval_point_rt<T, MAXN>(x[e], okl, okl ? n[e] : 0, ConstRows<T>{}, [&](int m, T v) {
+          if (wd) dst[m] = v;
+        });
       }
-      const bool okl = in && xok && n <= MAXN;
-      T* dst = out + goff;
-      eval_point_rt<T, MAXN>(x, okl, okl ? n : 0, ConstRows<T>{}, [&](int m, T v) {
-        if (in && n <= MAXN) dst[m] = v;
-      });
       continue;
     }
-    const bool ok = in && xok;
-    const T xs = ok ? x : A::nan();                // NaN propagates through the tail
-    const T xe = ok ? x : T(0);
-    const T t = exp_neg_clamped(xe);
-    const bool defer = ok && xe < rows(n).z;
-    const unsigned dmask = __ballot_sync(kFull, defer);
     // staging position matches the global 16-byte phase of the chunk range
     constexpr int Q = 16 / sizeof(T);
     const int shift = (int)(base & (Q - 1));
-    const int loc = (int)(goff - base) + shift;
     // the previous chunk's bulk store must have finished reading the slot
     if (lane == 0) bulk_wait_read<0>();
     __syncwarp();
-    T* dst = W.stage + loc;
-    if (dmask) {                                   // enqueue (qn stays warp-uniform)
-      if (defer) {
-        const int slot = qn + __popc(dmask & ((1u << lane) - 1u));
-        W.qx[slot] = xe;
-        W.qt[slot] = t;
-        W.qn[slot] = (unsigned char)n;
-        W.qoff[slot] = goff;
+    T xs[EPL], t[EPL], cur[EPL], tx[EPL];
+    T* dst[EPL];
+    bool wr[EPL];
+    int wmax_l = 0;
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) {
+      const bool ok = in[e] && xok[e];
+      xs[e] = ok ? x[e] : A::nan();                // NaN propagates through the tail
+      const T xe = ok ? x[e] : T(0);
+      t[e] = exp_neg_clamped(xe);
+      const bool defer = ok && xe < rows(n[e]).z;
+      const unsigned dmask = __ballot_sync(kFull, defer);
+      dst[e] = W.stage + (int)(goff[e] - base) + shift;
+      if (dmask) {                                 // enqueue (qn stays warp-uniform)
+        if (defer) {
+          const int slot = qn + __popc(dmask & ((1u << lane) - 1u));
+          W.qx[slot] = xe;
+          W.qt[slot] = t[e];
+          W.qn[slot] = (unsigned char)n[e];
+          W.qoff[slot] = goff[e];
+        }
+        qn += __popc(dmask);
       }
-      qn += __popc(dmask);
+      wr[e] = in[e] && !defer;
+      wmax_l = max(wmax_l, wr[e] ? n[e] : 0);
     }
     // immediate elements (past the cut-off): y = x.  Same operation sequence as
     // seed<T, n> + the recursion + the upward ladder.
     {
-      const bool wr = in && !defer;
-      const int wmax = __reduce_max_sync(kFull, (unsigned)(wr ? n : 0));
+      const int wmax = __reduce_max_sync(kFull, (unsigned)wmax_l);
       const int bits = 32 - __clz(wmax | 1);
-      const T r = A::rcp(xs);
-      const T sr = A::sqrt(r);
-      const T cn = rows(n).c;
-      // n = 0: powi gives exactly 1.0 and (c * 1.0) * sr == c * sr, so no select
-      T cur = A::mul(A::mul(cn, powi_rt_bounded(r, n, bits)), sr);
-      if (wr) dst[n] = cur;
-      const T tx = A::add(xs, xs);
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) {
+        const T r = A::rcp(xs[e]);
+        const T sr = A::sqrt(r);
+        const T cn = rows(n[e]).c;
+        // n = 0: powi gives exactly 1.0 and (c * 1.0) * sr == c * sr, so no select
+        cur[e] = A::mul(A::mul(cn, powi_rt_bounded(r, n[e], bits)), sr);
+        if (wr[e]) dst[e][n[e]] = cur[e];
+        tx[e] = A::add(xs[e], xs[e]);
+      }
       // recursion steps m = wmax-1 .. 0: enter the unrolled chain once through
       // a jump table (wmax is warp-uniform) instead of testing every step
-#define BOYS_STEP(M)                                                     \
-  if ((M) < NB) {                                                         \
-    const T nx = A::mul(A::fma(tx, cur, t), rinv<T>((M) < NB ? (M) : 0)); \
-    const bool on = (M) < n;                                              \
-    pmov(on, cur, nx);                                                    \
-    psts(on && wr, dst + (M), cur);                                       \
+#define BOYS_STEP(M)                                                       \
+  if ((M) < NB) {                                                           \
+    _Pragma("unroll") for (int e = 0; e < EPL; ++e) {                       \
+      const T nx = A::mul(A::fma(tx[e], cur[e], t[e]), rinv<T>((M) < NB ? (M) : 0)); \
+      const bool on = (M) < n[e];                                           \
+      pmov(on, cur[e], nx);                                                 \
+      psts(on && wr[e], dst[e] + (M), cur[e]);                              \
+    }                                                                       \
   }
       switch (wmax) {
         case 16: BOYS_STEP(15) [[fallthrough]];
@@ -554,16 +599,24 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
       }
 #undef BOYS_STEP
       static_assert(NB <= 16, "extend the recursion jump table");
-      const bool up = wr && ok && xs > rows(n).x_up;
-      if (__any_sync(kFull, up)) {
-        const T rx = A::rcp(xs);
-        T f = up_first(xs);
-        if (up) dst[0] = f;
+      bool up[EPL], anyup = false;
 #pragma unroll
-        for (int m = 0; m < NB; ++m) {
-          if (m >= wmax) break;
-          f = up_next(f, m, rx);
-          if (up && m + 1 <= n) dst[m + 1] = f;
+      for (int e = 0; e < EPL; ++e) {
+        up[e] = wr[e] && xs[e] > rows(n[e]).x_up;   // NaN (invalid) compares false
+        anyup = anyup || up[e];
+      }
+      if (__any_sync(kFull, anyup)) {
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) {
+          const T rx = A::rcp(xs[e]);
+          T f = up_first(xs[e]);
+          if (up[e]) dst[e][0] = f;
+#pragma unroll
+          for (int m = 0; m < NB; ++m) {
+            if (m >= wmax) break;
+            f = up_next(f, m, rx);
+            if (up[e] && m + 1 <= n[e]) dst[e][m + 1] = f;
+          }
         }
       }
     }
@@ -584,7 +637,7 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
         if (lane == 0) bulk_store(out + base + head, W.stage + shift + head, body * sizeof(T));
       }
     }
-    if (qn >= 32) ragged_drain<T, NB>(W, rows, qn, lane, out);
+    while (qn >= 32) ragged_drain<T, NB>(W, rows, qn, lane, out);
   }
   while (qn > 0) ragged_drain<T, NB>(W, rows, qn, lane, out);
   if (lane == 0) bulk_wait_all();
@@ -1100,16 +1153,15 @@ static boys_status dispatch_split(int nn, int nbar, const void* x, int64_t N, vo
   }
 }
 
-// Ragged kernel per dtype, chosen by same-box measurement on B200 (cfg4):
-//   f32: block windows 1.19 ms vs warp chunks 1.52 ms  -> windows
-//   f64: block windows 2.59 ms vs warp chunks 2.24 ms  -> warp chunks
+// Ragged kernel, chosen by same-box measurement on B200 (cfg4):
+//   f32: block windows 1.19 ms vs warp chunks 1.14 ms (4 elements per lane)
+//   f64: block windows 2.59 ms vs warp chunks 1.95 ms (3 elements per lane)
 // (f64's heavier below-cut-off tasks leave the window barriers waiting).
-// BOYS_RAGGED_WIN=0/1 forces one kernel for both dtypes.
+// BOYS_RAGGED_WIN=1 selects the window kernel (A/B).
 template <typename T>
 static bool ragged_win() {
   static int v = env_int("BOYS_RAGGED_WIN", -1);
-  if (v == 0 || v == 1) return v == 1;
-  return sizeof(T) == 4;
+  return v == 1;          // default: warp chunks (faster for both dtypes)
 }
 
 template <typename T, int NB, int WT>
@@ -1130,6 +1182,24 @@ static boys_status launch_win(const void* x, const uint8_t* nm, const int64_t* o
   return cuda_status(cudaGetLastError());
 }
 
+static int ragged_epl() {   // BOYS_RAGGED_EPL=1: one element per lane (A/B)
+  static int v = env_int("BOYS_RAGGED_EPL", 0);
+  return v;
+}
+
+template <typename T, int NB, int EPL>
+static boys_status launch_chunks(const void* x, const uint8_t* nm, const int64_t* off, int64_t N,
+                                 void* out, int64_t* dom, cudaStream_t s) {
+  auto k = ragged_kernel<T, NB, EPL>;
+  const size_t smem = sizeof(RaggedSmem<T, NB, EPL>);
+  static std::atomic<uint64_t> attr_mask{0};
+  boys_status st = opt_in_smem(k, (int)smem, attr_mask);
+  if (st != BOYS_OK) return st;
+  const int64_t nch = (N + 32 * EPL - 1) / (32 * EPL);
+  k<<<blocks_for(k, smem, (nch + 7) / 8), kThreads, smem, s>>>((const T*)x, nm, off, N, (T*)out, dom);
+  return BOYS_OK;
+}
+
 template <typename T>
 static boys_status launch_ragged(const void* x, const uint8_t* nm, const int64_t* off, int64_t N,
                                  void* out, int64_t* dom, cudaStream_t s) {
@@ -1143,13 +1213,12 @@ static boys_status launch_ragged(const void* x, const uint8_t* nm, const int64_t
     if (st != BOYS_OK) return st;
   } else {
     // (order-sorted warp super-chunks were measured slower: 2.90 / 3.79 ms vs 2.42)
-    auto k = ragged_kernel<T, NB>;
-    const size_t smem = sizeof(RaggedSmem<T, NB>);
-    static std::atomic<uint64_t> attr_mask{0};
-    boys_status st = opt_in_smem(k, (int)smem, attr_mask);
+    // elements per lane: measured best 3 (f64: 1.95 ms vs 2.27 / 1.97 / 2.05
+    // for 1 / 2 / 4) and 4 (f32: 1.14 ms vs 1.26 / 1.16 / 1.36 for 2 / 3 / 6)
+    constexpr int EPL = sizeof(T) == 8 ? 3 : 4;
+    boys_status st = ragged_epl() == 1 ? launch_chunks<T, NB, 1>(x, nm, off, N, out, dom, s)
+                                       : launch_chunks<T, NB, EPL>(x, nm, off, N, out, dom, s);
     if (st != BOYS_OK) return st;
-    const int64_t nch = (N + 31) / 32;
-    k<<<blocks_for(k, smem, (nch + 7) / 8), kThreads, smem, s>>>((const T*)x, nm, off, N, (T*)out, dom);
   }
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cuda_status(cudaGetLastError());

@@ -174,6 +174,28 @@ def test_ragged_bit_exact_and_equals_dense(oracle, dtype, cap):
             assert np.array_equal(got[roff[i]:roff[i + 1]], d[j], equal_nan=True)
 
 
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_ragged_uniform_orders_staging_capacity(oracle, dtype):
+    """Chunks whose output range fills the warp staging exactly (12 values per
+    element) or overflows it (orders 12..16: per-element direct-write path),
+    plus runs of high orders clustered between low ones and ragged tails."""
+    rng = np.random.default_rng(11)
+    mx = max_order(dtype)
+    cases = [np.full(4000, n, np.uint8) for n in (0, 10, 11, 12, mx)]
+    cl = rng.integers(0, 3, 5000).astype(np.uint8)
+    cl[1000:1400] = mx                                   # a cluster of high orders
+    cl[3000:3100] = 11
+    cases.append(cl)
+    for nm in cases:
+        for N in (nm.size, nm.size - 37):                # full and ragged last chunk
+            nmv = nm[:N]
+            x = dense_inputs(dtype, int(nmv.max()), N=N)[:N]
+            got, off = boys_ragged(torch.from_numpy(x).cuda(), torch.from_numpy(nmv).cuda())
+            ref, roff, bad = oracle.ragged(x, nmv)
+            assert bad == -1
+            assert_parity(got.cpu().numpy(), ref, f"ragged uniform {dtype.__name__}")
+
+
 def test_ragged_cfg4_inputs(oracle):
     x, nm = W.cfg4_batch(1 << 20, device="cuda")
     got, off = boys_ragged(x, nm)
