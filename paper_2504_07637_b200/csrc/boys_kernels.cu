@@ -381,13 +381,11 @@ __device__ __forceinline__ void eval_point_rt(T x_in, bool ok, int n, const Rows
 // by EPL elements per lane, whose independent chains also interleave (ILP).
 // Staging holds CAP values; a chunk whose output range exceeds it takes the
 // per-element direct-write path (never for ERI-like order mixes).
-template <int NB, int EPL> struct RaggedCap {
-  static constexpr int value = EPL == 1 ? 32 * (NB + 1) : 32 * EPL * (NB < 11 ? NB + 1 : 12);
-};
-
-template <typename T, int NB, int EPL>
+// CPE: staging values per element (NB + 1 = no overflow possible).
+// MINB: __launch_bounds__ min blocks per SM (0 = unconstrained).
+template <typename T, int NB, int EPL, int CPE>
 struct RaggedWarp {
-  static constexpr int CAP = RaggedCap<NB, EPL>::value;
+  static constexpr int CAP = 32 * EPL * (CPE < NB + 1 ? CPE : NB + 1);
   static constexpr int QCAP = 32 * EPL + 32;      // < 32 left after a drain + one chunk
   alignas(16) T stage[CAP + 16 / sizeof(T)];
   T qx[QCAP], qt[QCAP];
@@ -396,10 +394,10 @@ struct RaggedWarp {
   T scratch[32];
 };
 
-template <typename T, int NB, int EPL>
+template <typename T, int NB, int EPL, int CPE>
 struct RaggedSmem {
   SmemTable<T, NB + 1> st;           // rows 0..NB (the fast path's orders)
-  RaggedWarp<T, NB, EPL> w[kThreads / 32];
+  RaggedWarp<T, NB, EPL, CPE> w[kThreads / 32];
 };
 
 // Evaluate up to 32 queued below-cut-off elements (one per lane), writing
@@ -440,16 +438,16 @@ template <> struct Sentinel<float> {
   static __device__ __forceinline__ bool is(float v) { return __float_as_int(v) == 0x7fa0c0de; }
 };
 
-template <typename T, int NB, int EPL>
-__global__ void __launch_bounds__(kThreads)
+template <typename T, int NB, int EPL, int CPE, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
 ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
               const int64_t* __restrict__ OFF, int64_t N, T* __restrict__ out,
               int64_t* __restrict__ dom) {
   using A = Ar<T>;
-  using WarpT = RaggedWarp<T, NB, EPL>;
+  using WarpT = RaggedWarp<T, NB, EPL, CPE>;
   constexpr int CH = 32 * EPL;                   // elements per chunk
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  RaggedSmem<T, NB, EPL>& S = *reinterpret_cast<RaggedSmem<T, NB, EPL>*>(smem_raw);
+  RaggedSmem<T, NB, EPL, CPE>& S = *reinterpret_cast<RaggedSmem<T, NB, EPL, CPE>*>(smem_raw);
   stage_table(S.st);
   __syncthreads();
   const SmemRows<T> rows{S.st.row};
@@ -1187,11 +1185,11 @@ static int ragged_epl() {   // BOYS_RAGGED_EPL=1: one element per lane (A/B)
   return v;
 }
 
-template <typename T, int NB, int EPL>
+template <typename T, int NB, int EPL, int CPE, int MINB>
 static boys_status launch_chunks(const void* x, const uint8_t* nm, const int64_t* off, int64_t N,
                                  void* out, int64_t* dom, cudaStream_t s) {
-  auto k = ragged_kernel<T, NB, EPL>;
-  const size_t smem = sizeof(RaggedSmem<T, NB, EPL>);
+  auto k = ragged_kernel<T, NB, EPL, CPE, MINB>;
+  const size_t smem = sizeof(RaggedSmem<T, NB, EPL, CPE>);
   static std::atomic<uint64_t> attr_mask{0};
   boys_status st = opt_in_smem(k, (int)smem, attr_mask);
   if (st != BOYS_OK) return st;
@@ -1216,8 +1214,11 @@ static boys_status launch_ragged(const void* x, const uint8_t* nm, const int64_t
     // elements per lane: measured best 3 (f64: 1.95 ms vs 2.27 / 1.97 / 2.05
     // for 1 / 2 / 4) and 4 (f32: 1.14 ms vs 1.26 / 1.16 / 1.36 for 2 / 3 / 6)
     constexpr int EPL = sizeof(T) == 8 ? 3 : 4;
-    boys_status st = ragged_epl() == 1 ? launch_chunks<T, NB, 1>(x, nm, off, N, out, dom, s)
-                                       : launch_chunks<T, NB, EPL>(x, nm, off, N, out, dom, s);
+    // (8 instead of 12 staged values per element, or a 3-blocks/SM register
+    // bound, measured no better: 1.96 / 2.08 ms f64)
+    boys_status st = ragged_epl() == 1
+                         ? launch_chunks<T, NB, 1, NB + 1, 0>(x, nm, off, N, out, dom, s)
+                         : launch_chunks<T, NB, EPL, 12, 0>(x, nm, off, N, out, dom, s);
     if (st != BOYS_OK) return st;
   }
   g_launches.fetch_add(1, std::memory_order_relaxed);
