@@ -293,12 +293,13 @@ __device__ __forceinline__ T y_below_rt(T x, T t, int n, const Rows& rows) {
 template <typename T>
 __device__ __forceinline__ T powi_rt_bounded(T b, int n, int bits) {
   using A = Ar<T>;
-  T r = T(1), p = b;
+  // j = 0: 1.0 * b == b exactly, so a select (n < 2^bits with bits >= 1)
+  T r = (n & 1) ? b : T(1), p = b;
 #pragma unroll
-  for (int j = 0; j < 6; ++j) {
+  for (int j = 1; j < 6; ++j) {
     if (j >= bits) break;
+    p = A::mul(p, p);
     r = A::mul(r, ((n >> j) & 1) ? p : T(1));
-    p = A::mul(p, p);      // unused past the top bit of n: no effect on r
   }
   return r;
 }
@@ -463,10 +464,12 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
   int64_t poff[EPL], pbase = 0, plast_off = 0;
   auto load = [&](int64_t cc) {
     const int64_t j0 = cc * CH;
+    // elements of chunk cc that exist (warp-uniform, 0 past the end)
+    const int rem = cc < nchunks ? (int)((N - j0) < CH ? (N - j0) : CH) : 0;
 #pragma unroll
     for (int e = 0; e < EPL; ++e) {
       const int64_t j = j0 + 32 * e + lane;
-      const bool jin = cc < nchunks && j < N;
+      const bool jin = 32 * e + lane < rem;
       px[e] = jin ? ldg_nc(X + j) : T(0);
       pn[e] = jin ? (int)NM[j] : 0;
       poff[e] = jin ? __ldg(OFF + j) : 0;
@@ -483,12 +486,13 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
     int n[EPL];
     int64_t goff[EPL];
     bool in[EPL];
+    const int rem = (int)((N - i0) < CH ? (N - i0) : CH);
 #pragma unroll
     for (int e = 0; e < EPL; ++e) {
       x[e] = px[e];
       n[e] = pn[e];
       goff[e] = poff[e];
-      in[e] = i0 + 32 * e + lane < N;
+      in[e] = 32 * e + lane < rem;
     }
     const int64_t base = pbase, cnt = plast_off - pbase;
     load(c + wstride);
