@@ -395,9 +395,12 @@ struct RaggedWarp {
   T scratch[32];
 };
 
+template <typename T> struct alignas(4 * sizeof(T)) ZcRow { T z, c, x_up, pad; };
+
 template <typename T, int NB, int EPL, int CPE>
 struct RaggedSmem {
   SmemTable<T, NB + 1> st;           // rows 0..NB (the fast path's orders)
+  ZcRow<T> zc[NB + 1];               // per-order scalars, one 16/32-byte line each
   RaggedWarp<T, NB, EPL, CPE> w[kThreads / 32];
 };
 
@@ -450,6 +453,8 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
   extern __shared__ __align__(128) unsigned char smem_raw[];
   RaggedSmem<T, NB, EPL, CPE>& S = *reinterpret_cast<RaggedSmem<T, NB, EPL, CPE>*>(smem_raw);
   stage_table(S.st);
+  for (int k = threadIdx.x; k <= NB; k += blockDim.x)
+    S.zc[k] = ZcRow<T>{Tab<T>::row(k).z, Tab<T>::row(k).c, Tab<T>::row(k).x_up, T(0)};
   __syncthreads();
   const SmemRows<T> rows{S.st.row};
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -529,6 +534,7 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
     if (lane == 0) bulk_wait_read<0>();
     __syncwarp();
     T xs[EPL], t[EPL], cur[EPL], tx[EPL];
+    ZcRow<T> zc[EPL];
     T* dst[EPL];
     bool wr[EPL];
     int wmax_l = 0;
@@ -538,7 +544,8 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
       xs[e] = ok ? x[e] : A::nan();                // NaN propagates through the tail
       const T xe = ok ? x[e] : T(0);
       t[e] = exp_neg_clamped(xe);
-      const bool defer = ok && xe < rows(n[e]).z;
+      zc[e] = S.zc[n[e]];
+      const bool defer = ok && xe < zc[e].z;
       const unsigned dmask = __ballot_sync(kFull, defer);
       dst[e] = W.stage + (int)(goff[e] - base) + shift;
       if (dmask) {                                 // enqueue (qn stays warp-uniform)
@@ -563,7 +570,7 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
       for (int e = 0; e < EPL; ++e) {
         const T r = A::rcp(xs[e]);
         const T sr = A::sqrt(r);
-        const T cn = rows(n[e]).c;
+        const T cn = zc[e].c;
         // n = 0: powi gives exactly 1.0 and (c * 1.0) * sr == c * sr, so no select
         cur[e] = A::mul(A::mul(cn, powi_rt_bounded(r, n[e], bits)), sr);
         if (wr[e]) dst[e][n[e]] = cur[e];
@@ -604,7 +611,7 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
       bool up[EPL], anyup = false;
 #pragma unroll
       for (int e = 0; e < EPL; ++e) {
-        up[e] = wr[e] && xs[e] > rows(n[e]).x_up;   // NaN (invalid) compares false
+        up[e] = wr[e] && xs[e] > zc[e].x_up;   // NaN (invalid) compares false
         anyup = anyup || up[e];
       }
       if (__any_sync(kFull, anyup)) {
