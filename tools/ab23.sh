@@ -1,0 +1,19 @@
+# A/B: ragged chunks with order-class rows (BOYS_RAGGED_EPL=7) vs default
+mkdir -p gpurun_out
+out=gpurun_out/ab.txt; : > $out
+for v in 7; do
+  BOYS_RAGGED_EPL=$v timeout 400 python -m pytest tests/test_gpu_parity.py tests/test_gpu_properties.py -x -q -m gpu -k "ragged" > gpurun_out/pytest_v$v.log 2>&1
+  echo "V=$v pytest rc=$?" >> $out; tail -n 1 gpurun_out/pytest_v$v.log >> $out
+done
+grep -q "rc=[1-9]" $out && { cat $out; exit 1; }
+run() {
+  local cfg=$1; shift
+  local line
+  line=$(env "$@" timeout 120 python bench.py --config $cfg --steps 100 --warmup 5 --no-extras --e2e-steps 0 --cpu-seconds 0 2>&1 | grep '^{')
+  echo "$cfg $* :: $(echo "$line" | python3 -c 'import json,sys; d=json.loads(sys.stdin.read()); r=d["roofline"]; print("frac=%.4f launch_ms=%.4f" % (r["frac"], r["launch_ms"]))')" >> $out
+}
+for rep in 1 2; do for v in 0 7; do
+  run cfg4 BOYS_RAGGED_EPL=$v
+  run cfg4f32 BOYS_RAGGED_EPL=$v
+done; done
+cat $out
