@@ -80,6 +80,16 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 
 template <typename T> __device__ __forceinline__ T ldg_nc(const T* p) { return __ldg(p); }
 
+// Programmatic dependent launch (launches with the programmatic-serialization
+// attribute): wait until the stream's previous grid has completed and its
+// memory is visible (a no-op for a normally serialised launch), then allow
+// the stream's next grid to be scheduled onto SM slots as ours free up --
+// only its launch and prologue overlap our tail; it waits the same way.
+__device__ __forceinline__ void pdl_wait_and_release() {
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+
 // Predicated move / shared store (inline PTX so the compiler keeps plain
 // predication instead of a divergent branch per recursion step).
 __device__ __forceinline__ void pmov(bool p, double& dst, double v) {
@@ -154,6 +164,7 @@ dense_kernel(const T* __restrict__ X, int64_t N, T* __restrict__ out, T* __restr
   T* sbase = reinterpret_cast<T*>(smem_raw);
   const int tid = threadIdx.x;
   const int64_t ntiles = (N + kThreads - 1) / kThreads;
+  pdl_wait_and_release();
   int it = 0;
   // x of the block's next tile is loaded one iteration ahead (its latency
   // overlaps this tile's arithmetic)
@@ -1132,6 +1143,10 @@ static int soa_small_minb() {   // BOYS_SOA0_MINB: 8 (default) or 6 for n <= 1
   static int v = env_int("BOYS_SOA0_MINB", 8) == 6 ? 6 : 8;
   return v;
 }
+static int pdl() {   // BOYS_PDL=0: plain stream-serialised launches (A/B)
+  static int v = env_int("BOYS_PDL", 1);
+  return v;
+}
 static int aos_minb() {
   static int v = env_int("BOYS_AOS_MINB", 4) == 6 ? 6 : 4;
   return v;
@@ -1158,7 +1173,22 @@ static boys_status launch_dense_k(const T* x, int64_t N, T* out, T* expx, int64_
   // tail) instead of the persistent grid -- A/B knob for small batches
   int grid = blocks_for(k, smem, ntiles);
   if (grid_tiles() && ntiles <= (int64_t)1 << 30) grid = (int)ntiles;
-  k<<<grid, kThreads, smem, s>>>(x, N, out, expx, dom, base, bulk_ok, soa_bulk);
+  if (pdl()) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k, x, N, out, expx, dom, base, bulk_ok, soa_bulk);
+    if (e != cudaSuccess) return cuda_status(e);
+  } else {
+    k<<<grid, kThreads, smem, s>>>(x, N, out, expx, dom, base, bulk_ok, soa_bulk);
+  }
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cuda_status(cudaGetLastError());
 }
