@@ -1169,10 +1169,18 @@ static boys_status launch_dense_k(const T* x, int64_t N, T* out, T* expx, int64_
   }
   int64_t ntiles = (N + kThreads - 1) / kThreads;
   bool bulk_ok = (reinterpret_cast<uintptr_t>(out) % 16) == 0;
-  // BOYS_GRID_TILES=1: one block per tile (the block scheduler balances the
-  // tail) instead of the persistent grid -- A/B knob for small batches
+  // Grid: persistent (SMs x resident blocks) or one block per tile, chosen
+  // by same-box measurement (tools/ab/ab29.sh, ab30.sh; graph-replayed
+  // streams at 2^20..2^24 points): one block per tile wins for f64 SoA at
+  // n <= 5 and n >= 11 (n=0: 143 vs 154 us, n=16: 398 vs 471 us at 2^24),
+  // persistent for f64 SoA n = 6..10 (n=8: 265 vs 282 us), for f32 SoA and for
+  // AoS (whose double-buffered bulk stores need the loop).  BOYS_GRID_TILES=1/2
+  // forces one or the other.
   int grid = blocks_for(k, smem, ntiles);
-  if (grid_tiles() && ntiles <= (int64_t)1 << 30) grid = (int)ntiles;
+  const int gt = grid_tiles();
+  const bool per_tile = gt == 1 || (gt == 0 && !AOS && !soa_bulk && sizeof(T) == 8 &&
+                                    (n <= 5 || n >= 11));
+  if (per_tile && ntiles <= (int64_t)1 << 30) grid = (int)ntiles;
   if (pdl()) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
