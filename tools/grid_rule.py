@@ -16,7 +16,8 @@ CASES = [(0, "soa", 18), (0, "soa", 20), (0, "soa", 22), (0, "soa", 24),
          (4, "soa", 20), (8, "soa", 20), (8, "soa", 22), (16, "soa", 20)]
 if len(sys.argv) > 1:      # e.g. "0,2,4,6,8,10,12,16:22,24"
     ns, lgs = sys.argv[1].split(":")
-    CASES = [(int(n), "soa", int(lg)) for lg in lgs.split(",") for n in ns.split(",")]
+    LAY = os.environ.get("LAYOUT", "soa")
+    CASES = [(int(n), LAY, int(lg)) for lg in lgs.split(",") for n in ns.split(",")]
 DT = torch.float32 if os.environ.get("DTYPE") == "f32" else torch.float64
 for n, lay, lg in CASES:
     N = 1 << lg
@@ -24,7 +25,8 @@ for n, lay, lg in CASES:
     g = torch.Generator(device="cuda").manual_seed(n * 100 + lg)
     xs = [(torch.rand(N, dtype=torch.float64, device="cuda", generator=g) * 60).to(DT)
           for _ in range(rot)]
-    outs = [torch.empty((n + 1, N), dtype=DT, device="cuda") for _ in range(rot)]
+    shape = (n + 1, N) if lay == "soa" else (N, n + 1)
+    outs = [torch.empty(shape, dtype=DT, device="cuda") for _ in range(rot)]
     for x, o in zip(xs, outs):
         boys(n, x, layout=lay, out=o, check=False)
     torch.cuda.synchronize()
