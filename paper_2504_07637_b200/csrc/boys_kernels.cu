@@ -22,6 +22,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/boys.h"
@@ -149,6 +150,103 @@ __device__ __forceinline__ T eval_point_stream(T x_in, bool ok, Put&& put) {
 template <typename T, int n>
 __device__ __forceinline__ void eval_point(T x_in, bool ok, T (&Fv)[n + 1], T& t_out) {
   t_out = eval_point_stream<T, n>(x_in, ok, [&](int m, T v) { Fv[m] = v; });
+}
+
+// Two adjacent points per thread, evaluated in lockstep: per point the same
+// operation sequence as eval_point_stream (so the same bits); put(m, a, b)
+// receives F_m of both points at once so a SoA row takes one 16-byte store.
+// The warp-uniform shortcuts see 64 points instead of 32 (values unchanged).
+template <typename T, int n, typename Put, typename Put1>
+__device__ __forceinline__ void eval_pair_stream(T xa, T xb, bool oka, bool okb, T& ta_out,
+                                                 T& tb_out, Put&& put, Put1&& put1) {
+  using A = Ar<T>;
+  const BoysRow<T>& R = Tab<T>::row(n);
+  const T bad = A::nan();
+  T x[2] = {oka ? xa : bad, okb ? xb : bad};
+  const bool ok[2] = {oka, okb};
+  T t[2], cur[2], tx[2];
+  bool below = false, up = false;
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    t[j] = exp_neg_clamped(x[j]);
+    below = below || (ok[j] && x[j] < R.z);
+  }
+  const bool any_below = __any_sync(kFull, below);
+#pragma unroll
+  for (int j = 0; j < 2; ++j) cur[j] = seed<T, n>(x[j], t[j], any_below);
+  put(n, cur[0], cur[1]);
+#pragma unroll
+  for (int j = 0; j < 2; ++j) tx[j] = A::add(x[j], x[j]);
+#pragma unroll
+  for (int m = n - 1; m >= 0; --m) {
+#pragma unroll
+    for (int j = 0; j < 2; ++j) cur[j] = A::mul(A::fma(tx[j], cur[j], t[j]), rinv<T>(m));
+    put(m, cur[0], cur[1]);
+  }
+#pragma unroll
+  for (int j = 0; j < 2; ++j) up = up || (ok[j] && x[j] > R.x_up);
+  if (__any_sync(kFull, up)) {
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const bool upj = ok[j] && x[j] > R.x_up;
+      T rx = A::rcp(x[j]);
+      T f = up_first(x[j]);
+      if (upj) put1(j, 0, f);
+#pragma unroll
+      for (int m = 0; m < n; ++m) {
+        f = up_next(f, m, rx);
+        if (upj) put1(j, m + 1, f);
+      }
+    }
+  }
+  ta_out = oka ? t[0] : bad;
+  tb_out = okb ? t[1] : bad;
+}
+
+// SoA dense kernel, two adjacent points per thread (512-point tiles): x comes
+// in as one 16-byte load and every F_m row leaves as 16-byte streaming stores
+// (512 contiguous bytes per warp instruction, half the store instructions).
+// Requires N even and 16-byte aligned x/out/expx (host checks).
+template <typename T, int n, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
+dense_soa_pair_kernel(const T* __restrict__ X, int64_t N, T* __restrict__ out,
+                      T* __restrict__ expx, int64_t* __restrict__ dom, int64_t index_base) {
+  using V2 = typename std::conditional<sizeof(T) == 8, double2, float2>::type;
+  const int tid = threadIdx.x;
+  constexpr int TILE = 2 * kThreads;
+  const int64_t ntiles = (N + TILE - 1) / TILE;
+  pdl_wait_and_release();
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t i = tile * TILE + 2 * tid;     // even; N even => i + 1 < N iff i < N
+    const bool in = i < N;
+    V2 xv;
+    if (in) xv = __ldg(reinterpret_cast<const V2*>(X + i));
+    else { xv.x = T(0); xv.y = T(0); }
+    bool oka = valid_x(xv.x), okb = valid_x(xv.y);
+    if (in && !oka) flag_domain(dom, index_base + i);
+    if (in && !okb) flag_domain(dom, index_base + i + 1);
+    oka = oka || !in;
+    okb = okb || !in;
+    T* o = out + i;
+    T ta, tb;
+    eval_pair_stream<T, n>(
+        xv.x, xv.y, oka, okb, ta, tb,
+        [&](int m, T a, T b) {
+          V2 v;
+          v.x = a;
+          v.y = b;
+          if (in) __stcs(reinterpret_cast<V2*>(o + (int64_t)m * N), v);
+        },
+        [&](int j, int m, T v) {
+          if (in) __stcs(o + (int64_t)m * N + j, v);
+        });
+    if (expx && in) {
+      V2 tv;
+      tv.x = ta;
+      tv.y = tb;
+      __stcs(reinterpret_cast<V2*>(expx + i), tv);
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1143,6 +1241,20 @@ static int soa_small_minb() {   // BOYS_SOA0_MINB: 8 (default) or 6 for n <= 1
   static int v = env_int("BOYS_SOA0_MINB", 8) == 6 ? 6 : 8;
   return v;
 }
+static int soa_pair() {   // BOYS_SOA_PAIR=1: two adjacent points per thread (SoA)
+  static int v = env_int("BOYS_SOA_PAIR", 1);
+  return v;
+}
+// Grid for the paired SoA kernel (BOYS_PAIR_GRID: 0 = rule below, 1 = per
+// tile, 2 = persistent).  Same-box sweeps (tools/ab/ab33.sh, 2^24 points):
+// one block per 512-point tile wins for every f64 order (n=8: 230 vs 266 us,
+// n=12: 314 vs 371 us) and for f32 n >= 6 (n=8: 112 vs 132 us); persistent
+// for f32 n < 6 (n=4: 82 vs 90 us).
+static bool soa_pair_per_tile(bool f64, int n) {
+  static int v = env_int("BOYS_PAIR_GRID", 0);
+  if (v) return v == 1;
+  return f64 || n >= 6;
+}
 static int pdl() {   // BOYS_PDL=0: plain stream-serialised launches (A/B)
   static int v = env_int("BOYS_PDL", 1);
   return v;
@@ -1201,6 +1313,34 @@ static boys_status launch_dense_k(const T* x, int64_t N, T* out, T* expx, int64_
   return cuda_status(cudaGetLastError());
 }
 
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+template <typename T, int n>
+static boys_status launch_soa_pair(const T* x, int64_t N, T* out, T* expx, int64_t* dom,
+                                   int64_t base, cudaStream_t s) {
+  constexpr int MINB = n <= 1 ? 6 : BOYS_SOA_MINB;   // two chains: 8 blocks would spill at n = 0
+  auto k = dense_soa_pair_kernel<T, n, MINB>;
+  const int64_t ntiles = (N + 2 * kThreads - 1) / (2 * kThreads);
+  int grid = blocks_for(k, 0, ntiles);
+  const int gt = grid_tiles();
+  if ((gt == 1 || (gt == 0 && soa_pair_per_tile(sizeof(T) == 8, n))) && ntiles <= ((int64_t)1 << 30))
+    grid = (int)ntiles;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl() ? 1 : 0;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k, x, N, out, expx, dom, base);
+  if (e != cudaSuccess) return cuda_status(e);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cuda_status(cudaGetLastError());
+}
+
 template <typename T, int n, bool AOS>
 static boys_status launch_dense_t(const T* x, int64_t N, T* out, T* expx, int64_t* dom,
                                   int64_t base, cudaStream_t s) {
@@ -1210,6 +1350,8 @@ static boys_status launch_dense_t(const T* x, int64_t N, T* out, T* expx, int64_
     if constexpr (n <= 1) {          // small orders: register budget for 6 or 8 blocks/SM
       if (soa_small_minb() == 6) return launch_dense_k<T, n, false, 1, 6>(x, N, out, expx, dom, base, s);
     }
+    if (soa_pair() && N % 2 == 0 && aligned16(x) && aligned16(out) && (!expx || aligned16(expx)))
+      return launch_soa_pair<T, n>(x, N, out, expx, dom, base, s);
     return launch_dense_k<T, n, false, 1, (n <= 1 ? 8 : BOYS_SOA_MINB)>(x, N, out, expx, dom, base, s);
   } else {
     // double-buffer the AoS tile while two tiles fit in ~80 KB (n <= 18 in f64)
