@@ -1255,6 +1255,14 @@ static bool soa_pair_per_tile(bool f64, int n) {
   if (v) return v == 1;
   return f64 || n >= 6;
 }
+// Ragged grid = resident blocks x this (BOYS_RAGGED_GRID_MULT overrides).
+// Same-box sweep (tools/ab/ab35.sh, cfg4): f64 best persistent (x1: 1.90 ms;
+// x2 1.90, x4 1.91, x16 1.98); f32 best x4 (0.984 vs 1.007 ms at x1).
+static int ragged_grid_mult(bool f64) {
+  static int v = env_int("BOYS_RAGGED_GRID_MULT", 0);
+  if (v >= 1) return v;
+  return f64 ? 1 : 4;
+}
 static int pdl() {   // BOYS_PDL=0: plain stream-serialised launches (A/B)
   static int v = env_int("BOYS_PDL", 1);
   return v;
@@ -1458,7 +1466,11 @@ static boys_status launch_chunks(const void* x, const uint8_t* nm, const int64_t
   boys_status st = opt_in_smem(k, (int)smem, attr_mask);
   if (st != BOYS_OK) return st;
   const int64_t nch = (N + 32 * EPL - 1) / (32 * EPL);
-  k<<<blocks_for(k, smem, (nch + 7) / 8), kThreads, smem, s>>>((const T*)x, nm, off, N, (T*)out, dom);
+  const int64_t nblk = (nch + 7) / 8;
+  int64_t grid = blocks_for(k, smem, nblk);
+  grid *= ragged_grid_mult(sizeof(T) == 8);
+  if (grid > nblk) grid = nblk;
+  k<<<(int)grid, kThreads, smem, s>>>((const T*)x, nm, off, N, (T*)out, dom);
   return BOYS_OK;
 }
 
