@@ -109,6 +109,7 @@ __device__ __forceinline__ void psts(bool p, float* a, float v) {
 }
 
 
+
 // F_0..F_n for one point, handed to put(m, value) in the order n, n-1, .., 0
 // (then, for lanes past x_up, 0..n again with the upward values).  Returns
 // e^{-x}.  `ok` = x in the domain; other lanes produce NaN.  Lanes only
@@ -756,13 +757,18 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
       }
       // recursion steps m = wmax-1 .. 0: enter the unrolled chain once through
       // a jump table (wmax is warp-uniform) instead of testing every step
+      // one predicate per element and step: elements that are not written
+      // here (deferred, padding) take no steps (their cur is never used)
+      int neff[EPL];
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) neff[e] = wr[e] ? n[e] : 0;
 #define BOYS_STEP(M)                                                       \
   if ((M) < NB) {                                                           \
     _Pragma("unroll") for (int e = 0; e < EPL; ++e) {                       \
       const T nx = A::mul(A::fma(tx[e], cur[e], t[e]), rinv<T>((M) < NB ? (M) : 0)); \
-      const bool on = (M) < n[e];                                           \
+      const bool on = (M) < neff[e];                                        \
       pmov(on, cur[e], nx);                                                 \
-      psts(on && wr[e], dst[e] + (M), cur[e]);                              \
+      psts(on, dst[e] + (M), cur[e]);                                       \
     }                                                                       \
   }
       switch (wmax) {
