@@ -617,15 +617,27 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
   int64_t poff[EPL], pbase = 0, plast_off = 0;
   auto load = [&](int64_t cc) {
     const int64_t j0 = cc * CH;
-    // elements of chunk cc that exist (warp-uniform, 0 past the end)
-    const int rem = cc < nchunks ? (int)((N - j0) < CH ? (N - j0) : CH) : 0;
+    if (j0 + CH <= N) {                          // full chunk (warp-uniform): no predicates
+      const T* xp = X + j0 + lane;
+      const uint8_t* np = NM + j0 + lane;
+      const int64_t* op = OFF + j0 + lane;
 #pragma unroll
-    for (int e = 0; e < EPL; ++e) {
-      const int64_t j = j0 + 32 * e + lane;
-      const bool jin = 32 * e + lane < rem;
-      px[e] = jin ? ldg_nc(X + j) : T(0);
-      pn[e] = jin ? (int)NM[j] : 0;
-      poff[e] = jin ? __ldg(OFF + j) : 0;
+      for (int e = 0; e < EPL; ++e) {
+        px[e] = ldg_nc(xp + 32 * e);
+        pn[e] = (int)np[32 * e];
+        poff[e] = __ldg(op + 32 * e);
+      }
+    } else {
+      // elements of chunk cc that exist (warp-uniform, 0 past the end)
+      const int rem = cc < nchunks ? (int)(N - j0) : 0;
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) {
+        const int64_t j = j0 + 32 * e + lane;
+        const bool jin = 32 * e + lane < rem;
+        px[e] = jin ? ldg_nc(X + j) : T(0);
+        pn[e] = jin ? (int)NM[j] : 0;
+        poff[e] = jin ? __ldg(OFF + j) : 0;
+      }
     }
     if (cc < nchunks) {
       pbase = __ldg(OFF + j0);
