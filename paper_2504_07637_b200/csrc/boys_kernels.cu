@@ -46,6 +46,9 @@ constexpr unsigned kFull = 0xffffffffu;
 #ifndef BOYS_DENSE_PREFETCH_AOS
 #define BOYS_DENSE_PREFETCH_AOS 0   // same for AoS (A/B: cfg3 86% vs 94%)
 #endif
+#ifndef BOYS_FAST_CR
+#define BOYS_FAST_CR 0   // 1: ragged chunks use the branch-free CR rcp/sqrt fast paths (A/B: f64 1.88 vs 1.83 ms, slower)
+#endif
 #ifndef BOYS_RAGGED_EXPC
 #define BOYS_RAGGED_EXPC 0   // 1: ragged chunks compact e^{-x} to x <= XEXP (A/B: no gain, 1.93 vs 1.92 ms)
 #endif
@@ -757,13 +760,47 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
     {
       const int wmax = __reduce_max_sync(kFull, (unsigned)wmax_l);
       const int bits = 32 - __clz(wmax | 1);
+      T r[EPL], sr[EPL];
+#if BOYS_FAST_CR
+      // correctly rounded 1/x and sqrt through the branch-free fast paths for
+      // all EPL elements at once (interleaved chains); the rare slow-path
+      // lanes (x near 0 / the exponent limits, NaN) recompute with the intrinsics
+      {
+        bool slow = false;
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) {
+          bool s1;
+          r[e] = A::rcp_fast(xs[e], s1);
+          slow = slow || s1;
+        }
+        if (__any_sync(kFull, slow)) {
+#pragma unroll
+          for (int e = 0; e < EPL; ++e) r[e] = A::rcp(xs[e]);
+        }
+        slow = false;
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) {
+          bool s2;
+          sr[e] = A::sqrt_fast(r[e], s2);
+          slow = slow || s2;
+        }
+        if (__any_sync(kFull, slow)) {
+#pragma unroll
+          for (int e = 0; e < EPL; ++e) sr[e] = A::sqrt(r[e]);
+        }
+      }
+#else
 #pragma unroll
       for (int e = 0; e < EPL; ++e) {
-        const T r = A::rcp(xs[e]);
-        const T sr = A::sqrt(r);
+        r[e] = A::rcp(xs[e]);
+        sr[e] = A::sqrt(r[e]);
+      }
+#endif
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) {
         const T cn = zc[e].c;
         // n = 0: powi gives exactly 1.0 and (c * 1.0) * sr == c * sr, so no select
-        cur[e] = A::mul(A::mul(cn, powi_rt_bounded(r, n[e], bits)), sr);
+        cur[e] = A::mul(A::mul(cn, powi_rt_bounded(r[e], n[e], bits)), sr[e]);
         if (wr[e]) dst[e][n[e]] = cur[e];
         tx[e] = A::add(xs[e], xs[e]);
       }
