@@ -435,6 +435,32 @@ def e2e_dense(cfg_name, steps, dev):
                                     "(chunked H2D / kernel / D2H pipeline)"}
 
 
+def e2e_ragged(wl, steps):
+    """Host-buffer ragged path through the public API (C-ABI
+    boys_eval_ragged_host): pinned host x and orders in, pinned values out."""
+    from paper_2504_07637_b200 import boys_ragged
+    N = wl.x.numel()
+    total = int(wl.values_per_step)
+    eb = wl.x.element_size()
+    xh = torch.empty(N, dtype=wl.x.dtype, pin_memory=True)
+    xh.copy_(wl.x)
+    nh = torch.empty(N, dtype=torch.uint8, pin_memory=True)
+    nh.copy_(wl.nm)
+    oh = torch.empty(total, dtype=wl.x.dtype, pin_memory=True)
+    boys_ragged(xh, nh, out=oh, return_offsets=False)     # warm-up (allocates workspace)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        boys_ragged(xh, nh, out=oh, return_offsets=False)
+    torch.cuda.synchronize()
+    el = time.perf_counter() - t0
+    return {"value": steps * total / el, "unit": UNIT,
+            "h2d_bytes_per_step": N * (eb + 1), "d2h_bytes_per_step": total * eb,
+            "steps": steps, "path": "boys_ragged(pinned host x, pinned host n_max) -> "
+                                    "boys_eval_ragged_host (chunked H2D / offsets scan / "
+                                    "kernel / D2H pipeline)"}
+
+
 def golden_check(cfg_name, rank, ws, dev):
     """Max relative error vs refmath.boys_downward goldens (tests/golden,
     double-double), gathered over ranks with all_gather (1 fp64 per rank)."""
@@ -576,6 +602,11 @@ def main():
                                "l2": note}
                 if rot > 1:
                     extras[key]["launches_per_step"] = rot
+                if name in ("cfg4", "cfg4f32") and args.e2e_steps > 0:
+                    try:
+                        extras[key]["e2e"] = e2e_ragged(w2, max(1, args.e2e_steps))
+                    except Exception as ex:  # noqa: BLE001
+                        extras[key]["e2e"] = {"error": str(ex)[:200]}
                 del w2
                 torch.cuda.empty_cache()
             except Exception as ex:  # noqa: BLE001

@@ -98,6 +98,18 @@ boys_status boys_domain_result(const int64_t* dom_dev, int64_t* first_bad, void*
 boys_status boys_eval_dense_host(boys_dtype dtype, int n_max, const void* x_host, int64_t N,
                                  void* out_host, boys_layout layout, int64_t* first_bad);
 
+/* Host-buffer ragged entry (end-to-end path for ragged batches): x_host[N] and
+ * nmax_host[N] -> out_host, element i's F_0..F_{n_i} at its exclusive prefix
+ * offset sum_{j<i}(n_j + 1), pipelined over chunks (host->device copies, the
+ * device offsets scan, the ragged kernel, device->host copy).  out_capacity:
+ * values out_host holds (BOYS_E_ARG if below sum(n_i + 1)).  Blocks until
+ * done.  BOYS_E_DOMAIN (and *first_bad) for an invalid x or an order above
+ * boys_max_order.  Replaces the reference's host-side batch call for ragged
+ * work lists (SPEC.md:316-324 with per-element orders). */
+boys_status boys_eval_ragged_host(boys_dtype dtype, const void* x_host, const uint8_t* nmax_host,
+                                  int64_t N, void* out_host, int64_t out_capacity,
+                                  int64_t* first_bad);
+
 /* Number of kernel launches issued by this library in this process. */
 int64_t boys_launch_count(void);
 

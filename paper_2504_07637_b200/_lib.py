@@ -20,7 +20,7 @@ BOYS_SOA, BOYS_AOS = 0, 1
 # every symbol include/boys.h declares (tests check the export table)
 EXPORTS = (
     "boys_max_order", "boys_version", "boys_eval_dense", "boys_eval_ragged",
-    "boys_ragged_offsets", "boys_eval_split", "boys_domain_result", "boys_eval_dense_host",
+    "boys_ragged_offsets", "boys_eval_split", "boys_domain_result", "boys_eval_dense_host", "boys_eval_ragged_host",
     "boys_launch_count", "boys_status_str", "boys_last_cuda_error",
 )
 
@@ -66,6 +66,8 @@ def load(build_if_missing: bool = True) -> C.CDLL:
         L.boys_domain_result.argtypes = [vp, C.POINTER(i64), vp]
         L.boys_eval_dense_host.restype = i32
         L.boys_eval_dense_host.argtypes = [i32, i32, vp, i64, vp, i32, C.POINTER(i64)]
+        L.boys_eval_ragged_host.restype = i32
+        L.boys_eval_ragged_host.argtypes = [i32, vp, vp, i64, vp, i64, C.POINTER(i64)]
         L.boys_launch_count.restype = i64
         L.boys_status_str.restype = C.c_char_p
         L.boys_status_str.argtypes = [i32]

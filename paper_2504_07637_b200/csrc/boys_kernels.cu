@@ -1604,6 +1604,29 @@ static boys_status pipe_get(int dev, size_t bx, size_t bo, HostPipe** out) {
   return BOYS_OK;
 }
 
+// ragged host-buffer pipeline workspace (per device, grown on demand, reused)
+struct RaggedPipe {
+  int device = -1;
+  size_t cap_x = 0, cap_n = 0, cap_off = 0, cap_out = 0, cap_dom = 0;
+  void* dx[2] = {nullptr, nullptr};
+  uint8_t* dn[2] = {nullptr, nullptr};
+  int64_t* doff[2] = {nullptr, nullptr};
+  void* dout[2] = {nullptr, nullptr};
+  int64_t* ddom = nullptr;       // one first-bad index per chunk
+  cudaStream_t st[2] = {nullptr, nullptr};
+};
+static std::vector<RaggedPipe> g_rpipes;
+
+static cudaError_t grow(void** p, size_t& cap, size_t need) {
+  if (need <= cap) return cudaSuccess;
+  cudaFree(*p);
+  *p = nullptr;
+  cap = 0;
+  cudaError_t e = cudaMalloc(p, need);
+  if (e == cudaSuccess) cap = need;
+  return e;
+}
+
 }  // namespace boys
 
 using namespace boys;
@@ -1760,6 +1783,103 @@ boys_status boys_eval_dense_host(boys_dtype dtype, int n_max, const void* x_host
     if (first_bad) *first_bad = bad;
     return BOYS_E_DOMAIN;
   }
+  return BOYS_OK;
+}
+
+boys_status boys_eval_ragged_host(boys_dtype dtype, const void* x_host, const uint8_t* nmax_host,
+                                  int64_t N, void* out_host, int64_t out_capacity,
+                                  int64_t* first_bad) {
+  if (dtype != BOYS_F64 && dtype != BOYS_F32) return BOYS_E_DTYPE;
+  if (N < 0 || out_capacity < 0) return BOYS_E_ARG;
+  if (first_bad) *first_bad = -1;
+  if (N == 0) return BOYS_OK;
+  if (!x_host || !nmax_host || !out_host) return BOYS_E_ARG;
+  std::lock_guard<std::mutex> lk(g_pipe_mu);
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_status(e);
+  RaggedPipe* p = nullptr;
+  for (auto& q : g_rpipes)
+    if (q.device == dev) { p = &q; break; }
+  if (!p) {
+    g_rpipes.emplace_back();
+    p = &g_rpipes.back();
+    p->device = dev;
+    for (auto& st : p->st) {
+      e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+      if (e != cudaSuccess) return cuda_status(e);
+    }
+  }
+  const size_t es = dsize(dtype);
+  const int64_t chunk = N < (int64_t(1) << 22) ? N : (int64_t(1) << 22);
+  const int64_t nchunks = (N + chunk - 1) / chunk;
+  // per-chunk domain slots; x/n/offsets buffers sized once for the chunk
+  for (int k = 0; k < 2; ++k) {
+    size_t cx = p->cap_x, cn = p->cap_n, co = p->cap_off;
+    if ((e = grow(&p->dx[k], cx, chunk * es)) != cudaSuccess) return cuda_status(e);
+    if ((e = grow((void**)&p->dn[k], cn, chunk)) != cudaSuccess) return cuda_status(e);
+    if ((e = grow((void**)&p->doff[k], co, (chunk + 1) * sizeof(int64_t))) != cudaSuccess)
+      return cuda_status(e);
+    if (k == 1) { p->cap_x = cx; p->cap_n = cn; p->cap_off = co; }
+  }
+  if ((e = grow((void**)&p->ddom, p->cap_dom, nchunks * sizeof(int64_t))) != cudaSuccess)
+    return cuda_status(e);
+  e = cudaMemsetAsync(p->ddom, 0xff, nchunks * sizeof(int64_t), p->st[0]);
+  if (e != cudaSuccess) return cuda_status(e);
+  cudaEvent_t ev;
+  cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+  cudaEventRecord(ev, p->st[0]);
+  cudaStreamWaitEvent(p->st[1], ev, 0);
+  const uint8_t* nh = nmax_host;
+  int64_t base = 0;
+  boys_status st = BOYS_OK;
+  for (int64_t c = 0; c < nchunks && st == BOYS_OK; ++c) {
+    const int k = (int)(c & 1);
+    cudaStream_t s = p->st[k];
+    const int64_t i0 = c * chunk;
+    const int64_t cn = (N - i0) < chunk ? (N - i0) : chunk;
+    // the chunk's output length (host pass over its orders, overlapped with
+    // the device work already queued for earlier chunks)
+    int64_t total = cn;
+    for (int64_t i = 0; i < cn; ++i) total += nh[i0 + i];
+    if (base + total > out_capacity) { st = BOYS_E_ARG; break; }
+    if ((size_t)total * es > p->cap_out) {     // grow both output slots (rare)
+      for (auto ss : p->st) cudaStreamSynchronize(ss);
+      size_t need = (size_t)total * es + (size_t)total * es / 4;
+      for (int q = 0; q < 2; ++q) {
+        size_t cap = p->cap_out;
+        if ((e = grow(&p->dout[q], cap, need)) != cudaSuccess) { st = cuda_status(e); break; }
+        if (q == 1) p->cap_out = cap;
+      }
+      if (st != BOYS_OK) break;
+    }
+    e = cudaMemcpyAsync(p->dx[k], (const char*)x_host + i0 * es, cn * es, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(p->dn[k], nh + i0, cn, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) { st = cuda_status(e); break; }
+    st = boys_ragged_offsets(p->dn[k], cn, p->doff[k], s);
+    if (st != BOYS_OK) break;
+    st = dtype == BOYS_F64
+             ? launch_ragged<double>(p->dx[k], p->dn[k], p->doff[k], cn, p->dout[k], p->ddom + c, s)
+             : launch_ragged<float>(p->dx[k], p->dn[k], p->doff[k], cn, p->dout[k], p->ddom + c, s);
+    if (st != BOYS_OK) break;
+    e = cudaMemcpyAsync((char*)out_host + base * es, p->dout[k], total * es, cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) { st = cuda_status(e); break; }
+    base += total;
+  }
+  for (auto s : p->st) {
+    e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess && st == BOYS_OK) st = cuda_status(e);
+  }
+  cudaEventDestroy(ev);
+  if (st != BOYS_OK) return st;
+  std::vector<int64_t> dom(nchunks);
+  e = cudaMemcpy(dom.data(), p->ddom, nchunks * sizeof(int64_t), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_status(e);
+  for (int64_t c = 0; c < nchunks; ++c)
+    if (dom[c] >= 0) {
+      if (first_bad) *first_bad = c * chunk + dom[c];
+      return BOYS_E_DOMAIN;
+    }
   return BOYS_OK;
 }
 

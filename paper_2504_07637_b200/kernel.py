@@ -233,10 +233,64 @@ def ragged_offsets(n_max: torch.Tensor) -> torch.Tensor:
     return off
 
 
+def _boys_ragged_host(x, n_max, out, return_offsets: bool):
+    """Host buffers -> boys_eval_ragged_host (pipelined copies + kernel).  The
+    offsets are the exclusive prefix sum of n_max + 1 (include/boys.h)."""
+    was_tensor = isinstance(x, torch.Tensor)
+    xn = x.detach().cpu().numpy() if was_tensor else np.asarray(x)
+    if xn.dtype not in (np.float64, np.float32):
+        xn = xn.astype(np.float64)
+    xn = np.ascontiguousarray(xn.reshape(-1))
+    nn = n_max.detach().cpu().numpy() if isinstance(n_max, torch.Tensor) else np.asarray(n_max)
+    nn = np.ascontiguousarray(nn.reshape(-1))
+    if nn.dtype != np.uint8 or nn.size != xn.size:
+        raise ValueError("n_max must be a uint8 array with one entry per x")
+    N = xn.size
+    if out is None:
+        res = np.empty(int(nn.sum(dtype=np.int64)) + N, dtype=xn.dtype)
+    else:
+        res = out.numpy() if isinstance(out, torch.Tensor) else out
+        if res.dtype != xn.dtype or res.ndim != 1 or not res.flags.c_contiguous:
+            raise ValueError(f"out must be a contiguous 1-D {xn.dtype} array")
+    if not torch.cuda.is_available():
+        raise RuntimeError("libboys needs a CUDA device (there is no CPU implementation)")
+    first = C.c_int64(-1)
+    code = L.load().boys_eval_ragged_host(
+        L.BOYS_F64 if xn.dtype == np.float64 else L.BOYS_F32, xn.ctypes.data_as(C.c_void_p),
+        nn.ctypes.data_as(C.c_void_p), N, res.ctypes.data_as(C.c_void_p), res.size, C.byref(first))
+    if code == L.BOYS_E_DOMAIN:
+        i = int(first.value)
+        mx = max_order(torch.float64 if xn.dtype == np.float64 else torch.float32)
+        if int(nn[i]) > mx:
+            raise ValueError(f"order {int(nn[i])} at index {i} exceeds the supported maximum {mx}")
+        bad = np.nonzero(~(np.isfinite(xn) & (xn >= 0)))[0]
+        raise ValueError(f"argument must be finite and >= 0; offending indices "
+                         f"{bad[:10].tolist()}" + (f" (and {bad.size - 10} more)"
+                                                     if bad.size > 10 else ""))
+    if code == L.BOYS_E_ARG and out is not None:
+        raise ValueError("out holds fewer values than sum(n_max + 1)")
+    L.check(code)
+    off = None
+    if return_offsets:
+        off = np.zeros(N + 1, dtype=np.int64)
+        np.cumsum(nn.astype(np.int64) + 1, out=off[1:])
+    vals = out if out is not None else (torch.from_numpy(res) if was_tensor else res)
+    if was_tensor and off is not None:
+        off = torch.from_numpy(off)
+    return vals, off
+
+
 def boys_ragged(x: torch.Tensor, n_max: torch.Tensor, offsets: torch.Tensor = None, *,
-                out: torch.Tensor = None, check: bool = True):
+                out: torch.Tensor = None, check: bool = True, return_offsets: bool = True):
     """Per-element orders: element i gets F_0..F_{n_max[i]}(x_i) at
-    values[offsets[i] : offsets[i+1]].  Returns (values, offsets)."""
+    values[offsets[i] : offsets[i+1]].  Returns (values, offsets).
+
+    x on a CUDA device: computed on the current stream (offsets as given, or
+    the exclusive prefix sum of n_max + 1).  x (and n_max) on the host: the
+    pipelined host-buffer path; results come back on the host, offsets are the
+    exclusive prefix sum (None with return_offsets=False)."""
+    if not (isinstance(x, torch.Tensor) and x.is_cuda):
+        return _boys_ragged_host(x, n_max, out, return_offsets)
     xf = _as_device_x(x)
     nm = n_max.contiguous().reshape(-1)
     if nm.dtype != torch.uint8 or nm.numel() != xf.numel() or nm.device != xf.device:

@@ -303,3 +303,44 @@ def test_concurrent_host_threads_and_streams():
     assert not errs, errs
     for k in range(len(xs)):
         assert torch.equal(res[k], serial[k]), f"thread {k}"
+
+
+def test_ragged_host_path(oracle):
+    """boys_eval_ragged_host: host x / orders in, host values out (several
+    pipeline chunks, both dtypes), bit-identical to the oracle and to the
+    device path; offsets = exclusive prefix sum of n + 1."""
+    for dtype in (torch.float64, torch.float32):
+        gen = W.cfg4f32_batch if dtype == torch.float32 else W.cfg4_batch
+        xr, nr = gen((1 << 22) + 4321, chunk=3)
+        xn, nn = xr.numpy(), nr.numpy()
+        vals, off = boys_ragged(xn, nn)
+        assert isinstance(vals, np.ndarray) and vals.dtype == xn.dtype
+        assert off[0] == 0 and off[-1] == vals.size
+        assert np.array_equal(np.diff(off), nn.astype(np.int64) + 1)
+        dv, doff = boys_ragged(xr.cuda(), nr.cuda())
+        assert np.array_equal(doff.cpu().numpy(), off)
+        assert_parity(vals, dv.cpu().numpy(), f"ragged host vs device {dtype}")
+        k = 1 << 16                                  # oracle on a prefix
+        ref, _, _ = oracle.ragged(xn[:k], nn[:k])
+        assert_parity(vals[: off[k]], ref, f"ragged host vs oracle {dtype}")
+        # caller-provided (pinned) output, no offsets
+        pin = torch.empty(vals.size, dtype=dtype, pin_memory=True)
+        got, none = boys_ragged(xr, nr, out=pin, return_offsets=False)
+        assert got is pin and none is None
+        assert np.array_equal(pin.numpy().view(np.uint8), vals.view(np.uint8))
+
+
+def test_ragged_host_errors():
+    x = np.array([1.0, 2.0, -3.0, 4.0])
+    n = np.array([0, 3, 1, 2], dtype=np.uint8)
+    with pytest.raises(ValueError, match=r"offending indices \[2\]"):
+        boys_ragged(x, n)
+    n2 = np.array([0, max_order(torch.float64) + 1, 1, 2], dtype=np.uint8)
+    with pytest.raises(ValueError, match="exceeds the supported maximum"):
+        boys_ragged(np.abs(x), n2)
+    with pytest.raises(ValueError, match="fewer values"):
+        boys_ragged(np.abs(x), n, out=np.empty(5))
+    with pytest.raises(ValueError, match="uint8"):
+        boys_ragged(np.abs(x), n.astype(np.int32))
+    vals, off = boys_ragged(np.zeros(0), np.zeros(0, dtype=np.uint8))
+    assert vals.size == 0 and off.tolist() == [0]
