@@ -40,17 +40,8 @@ constexpr int kRaggedFastOrders = 16;
 #define BOYS_SOA_MINB 4   // SoA resident-block target (register budget 64/thread)
 #endif
 constexpr unsigned kFull = 0xffffffffu;
-#ifndef BOYS_DENSE_PREFETCH_SOA
-#define BOYS_DENSE_PREFETCH_SOA 0   // 1: x of the next tile loaded ahead (A/B: cfg2 77% vs 84% HBM)
-#endif
-#ifndef BOYS_DENSE_PREFETCH_AOS
-#define BOYS_DENSE_PREFETCH_AOS 0   // same for AoS (A/B: cfg3 86% vs 94%)
-#endif
 #ifndef BOYS_FAST_CR
 #define BOYS_FAST_CR 0   // 1: ragged chunks use the branch-free CR rcp/sqrt fast paths (A/B: f64 1.88 vs 1.83 ms, slower)
-#endif
-#ifndef BOYS_RAGGED_EXPC
-#define BOYS_RAGGED_EXPC 0   // 1: ragged chunks compact e^{-x} to x <= XEXP (A/B: no gain, 1.93 vs 1.92 ms)
 #endif
 
 static std::atomic<int64_t> g_launches{0};
@@ -268,23 +259,13 @@ dense_kernel(const T* __restrict__ X, int64_t N, T* __restrict__ out, T* __restr
   const int64_t ntiles = (N + kThreads - 1) / kThreads;
   pdl_wait_and_release();
   int it = 0;
-  // x of the block's next tile is loaded one iteration ahead (its latency
-  // overlaps this tile's arithmetic)
-  constexpr bool kPf = AOS ? BOYS_DENSE_PREFETCH_AOS : BOYS_DENSE_PREFETCH_SOA;
-  T xnext = T(0);
-  if (kPf && (int64_t)blockIdx.x * kThreads + tid < N) xnext = ldg_nc(X + (int64_t)blockIdx.x * kThreads + tid);
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
     const int64_t i0 = tile * kThreads;
     const int64_t i = i0 + tid;
     const bool in = i < N;
-    T x;
-    if constexpr (kPf) {
-      x = in ? xnext : T(0);
-      const int64_t inx = i + (int64_t)gridDim.x * kThreads;
-      if (inx < N) xnext = ldg_nc(X + inx);
-    } else {
-      x = in ? ldg_nc(X + i) : T(0);
-    }
+    // (loading the next tile's x one iteration ahead measured slower:
+    // SoA 77% vs 84%, AoS 86% vs 94% of HBM, tools/ab/ab25.sh)
+    const T x = in ? ldg_nc(X + i) : T(0);
     bool ok = valid_x(x);
     if (in && !ok) flag_domain(dom, index_base + i);
     ok = ok || !in;   // tail lanes evaluate x = 0 quietly
@@ -701,41 +682,14 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
     T* dst[EPL];
     bool wr[EPL];
     int wmax_l = 0;
-#if BOYS_RAGGED_EXPC
-    // e^{-x} only where it is nonzero (x <= XEXP: ~28% of ERI-like elements),
-    // compacted to one lane per element: the chunk's list is staged in the
-    // (free) staging buffer, evaluated in place 32 at a time, and read back.
-    // Elsewhere t = 0 exactly, as exp_neg_clamped gives; invalid elements
-    // carry NaN x, so their t is never observable.
-    {
-      int ecnt = 0, epos[EPL];
-      bool eneed[EPL];
-      const unsigned lt = (1u << lane) - 1u;
-#pragma unroll
-      for (int e = 0; e < EPL; ++e) {
-        eneed[e] = in[e] && xok[e] && x[e] <= A::XEXP;
-        const unsigned em = __ballot_sync(kFull, eneed[e]);
-        epos[e] = ecnt + __popc(em & lt);
-        ecnt += __popc(em);
-        if (eneed[e]) W.stage[epos[e]] = x[e];
-      }
-      __syncwarp();
-      for (int b = 0; b < ecnt; b += 32)         // warp-uniform trip count
-        if (b + lane < ecnt) W.stage[b + lane] = A::exp_neg(W.stage[b + lane]);
-      __syncwarp();
-#pragma unroll
-      for (int e = 0; e < EPL; ++e) t[e] = eneed[e] ? W.stage[epos[e]] : T(0);
-      __syncwarp();                                // reads done before staging writes
-    }
-#endif
+    // (evaluating e^{-x} only for the elements with x <= XEXP, compacted one
+    // per lane, measured no faster: tools/ab/ab24.sh)
 #pragma unroll
     for (int e = 0; e < EPL; ++e) {
       const bool ok = in[e] && xok[e];
       xs[e] = ok ? x[e] : A::nan();                // NaN propagates through the tail
       const T xe = ok ? x[e] : T(0);
-#if !BOYS_RAGGED_EXPC
       t[e] = exp_neg_clamped(xe);
-#endif
       zc[e] = S.zc[n[e]];
       // deferred to the warp queue: below the cut-off (Q~ needed) and, in
       // fp32, above x_up (upward ladder)
