@@ -40,6 +40,9 @@ constexpr int kRaggedFastOrders = 16;
 #define BOYS_SOA_MINB 4   // SoA resident-block target (register budget 64/thread)
 #endif
 constexpr unsigned kFull = 0xffffffffu;
+#ifndef BOYS_PAIR_FASTCR
+#define BOYS_PAIR_FASTCR 0   // 1: paired SoA kernel shares fast-path checks for div/sqrt/rcp (A/B: slower, spills: cfg1 10.7 vs 9.5 us)
+#endif
 #ifndef BOYS_FAST_CR
 #define BOYS_FAST_CR 0   // 1: ragged chunks use the branch-free CR rcp/sqrt fast paths (A/B: f64 1.88 vs 1.83 ms, slower)
 #endif
@@ -147,6 +150,59 @@ __device__ __forceinline__ void eval_point(T x_in, bool ok, T (&Fv)[n + 1], T& t
   t_out = eval_point_stream<T, n>(x_in, ok, [&](int m, T v) { Fv[m] = v; });
 }
 
+// seed<double, n> for two points with the correctly rounded div / sqrt / rcp
+// taken through their branch-free fast paths (boys_eval.cuh, bit-identical to
+// the intrinsics): one warp vote per operation decides whether any lane needs
+// the intrinsic instead, so the two chains share one check per operation.
+template <int n>
+__device__ __forceinline__ void seed_pair(const double (&x)[2], const double (&t)[2],
+                                          bool any_below, double (&F)[2]) {
+  using A = Ar<double>;
+  const BoysRow<double>& R = Tab<double>::row(n);
+  double y[2] = {x[0], x[1]};
+  if (any_below) {
+    constexpr int LU = Tab<double>::shape(n, 0), lu = Tab<double>::shape(n, 1);
+    constexpr int LV = Tab<double>::shape(n, 2), lv = Tab<double>::shape(n, 3);
+    double u[2], v[2], w[2], Q[2], sq[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      u[j] = factored<double, LU, lu>(x[j], R.uq, R.ul);
+      v[j] = factored<double, LV, lv>(x[j], R.vq, R.vl);
+    }
+    bool s0, s1;
+    w[0] = A::div_fast(u[0], v[0], s0);
+    w[1] = A::div_fast(u[1], v[1], s1);
+    if (__any_sync(kFull, s0 || s1)) { w[0] = A::div(u[0], v[0]); w[1] = A::div(u[1], v[1]); }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      double h = A::mul(R.q2, w[j]);
+      h = A::fma(h, x[j], R.q1);
+      Q[j] = A::fma(h, x[j], R.q0);
+    }
+    sq[0] = A::sqrt_fast(Q[0], s0);
+    sq[1] = A::sqrt_fast(Q[1], s1);
+    if (__any_sync(kFull, s0 || s1)) { sq[0] = A::sqrt(Q[0]); sq[1] = A::sqrt(Q[1]); }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const double s = n == 0 ? sq[j] : A::mul(powi<double, (n == 0 ? 1 : n)>(Q[j]), sq[j]);
+      const double yq = A::fma(s, t[j], x[j]);
+      y[j] = x[j] < R.z ? yq : x[j];
+    }
+  }
+  double r[2], sr[2];
+  bool s0, s1;
+  r[0] = A::rcp_fast(y[0], s0);
+  r[1] = A::rcp_fast(y[1], s1);
+  if (__any_sync(kFull, s0 || s1)) { r[0] = A::rcp(y[0]); r[1] = A::rcp(y[1]); }
+  sr[0] = A::sqrt_fast(r[0], s0);
+  sr[1] = A::sqrt_fast(r[1], s1);
+  if (__any_sync(kFull, s0 || s1)) { sr[0] = A::sqrt(r[0]); sr[1] = A::sqrt(r[1]); }
+#pragma unroll
+  for (int j = 0; j < 2; ++j)
+    F[j] = n == 0 ? A::mul(R.c, sr[j])
+                  : A::mul(A::mul(R.c, powi<double, (n == 0 ? 1 : n)>(r[j])), sr[j]);
+}
+
 // Two adjacent points per thread, evaluated in lockstep: per point the same
 // operation sequence as eval_point_stream (so the same bits); put(m, a, b)
 // receives F_m of both points at once so a SoA row takes one 16-byte store.
@@ -167,8 +223,14 @@ __device__ __forceinline__ void eval_pair_stream(T xa, T xb, bool oka, bool okb,
     below = below || (ok[j] && x[j] < R.z);
   }
   const bool any_below = __any_sync(kFull, below);
+#if BOYS_PAIR_FASTCR
+  if constexpr (sizeof(T) == 8) seed_pair<n>(x, t, any_below, cur);
+  else
+#endif
+  {
 #pragma unroll
-  for (int j = 0; j < 2; ++j) cur[j] = seed<T, n>(x[j], t[j], any_below);
+    for (int j = 0; j < 2; ++j) cur[j] = seed<T, n>(x[j], t[j], any_below);
+  }
   put(n, cur[0], cur[1]);
 #pragma unroll
   for (int j = 0; j < 2; ++j) tx[j] = A::add(x[j], x[j]);
