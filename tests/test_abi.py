@@ -55,6 +55,17 @@ def test_argument_errors_without_gpu():
     bad = ctypes.c_void_p(x.ctypes.data + 4)
     assert L.boys_eval_dense(_lib.BOYS_F64, 2, bad, 4, p, 0, None, None, None) == _lib.BOYS_E_ALIGN
     assert L.boys_eval_split(_lib.BOYS_F64, 4, 4, p, 4, p, 0, None, None) == _lib.BOYS_E_ARG
+    # ragged host-buffer entry
+    n8 = np.zeros(4, dtype=np.uint8)
+    pn = n8.ctypes.data_as(ctypes.c_void_p)
+    fb = ctypes.c_int64(7)
+    assert L.boys_eval_ragged_host(9, p, pn, 4, p, 4, ctypes.byref(fb)) == _lib.BOYS_E_DTYPE
+    assert L.boys_eval_ragged_host(_lib.BOYS_F64, p, pn, -1, p, 4, None) == _lib.BOYS_E_ARG
+    assert L.boys_eval_ragged_host(_lib.BOYS_F64, p, pn, 4, p, -1, None) == _lib.BOYS_E_ARG
+    assert L.boys_eval_ragged_host(_lib.BOYS_F64, None, pn, 4, p, 4, None) == _lib.BOYS_E_ARG
+    assert L.boys_eval_ragged_host(_lib.BOYS_F64, p, None, 4, p, 4, None) == _lib.BOYS_E_ARG
+    assert L.boys_eval_ragged_host(_lib.BOYS_F64, p, pn, 0, p, 0, ctypes.byref(fb)) == _lib.BOYS_OK
+    assert fb.value == -1
 
 
 def test_no_cpu_fallback():
