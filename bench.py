@@ -359,18 +359,28 @@ def roofline_obj(wl, per_ms, hbm_peak, fp64_peak, bound=None, traffic=None):
 # CPU baseline / reference arm (oracle port on host cores)
 # ----------------------------------------------------------------------------
 
-def cpu_port_rate(n, x_host, layout, min_seconds=10.0):
+def cpu_port_rate(n, x_host, layout, min_seconds=10.0, gpu_out=None):
+    """Times the C restatement on the host cores.  gpu_out (the GPU's values for
+    the same sample): the baseline's own output is also the parity checker --
+    returns the max |GPU - CPU| in ulp over the sample (0 = bit-identical)."""
     from oracle import oracle as O
     O.dense(n, x_host[:1024], layout)      # load + warm
     t0 = time.perf_counter()
     reps = 0
+    ref = None
     while True:
-        O.dense(n, x_host, layout)
+        ref, _ = O.dense(n, x_host, layout)
         reps += 1
         el = time.perf_counter() - t0
         if el >= min_seconds:
             break
-    return reps * x_host.size * (n + 1) / el, O.threads(), reps
+    ulp = None
+    if gpu_out is not None:
+        a = gpu_out.view(np.int64).astype(np.int64)
+        b = ref.view(np.int64).astype(np.int64)
+        both_nan = np.isnan(gpu_out) & np.isnan(ref)
+        ulp = int(np.where(both_nan, 0, np.abs(a - b)).max(initial=0))
+    return reps * x_host.size * (n + 1) / el, O.threads(), reps, ulp
 
 
 def run_reference(args, rank, ws):
@@ -551,11 +561,15 @@ def main():
 
     # CPU baseline: the C oracle on the host cores, rank 0 at N=1 only
     if rank == 0 and ws == 1 and cfg.layout != "ragged" and args.cpu_seconds > 0:
-        xs = wl.xs[0][: 1 << 21].cpu().numpy()
-        v, cores, reps = cpu_port_rate(cfg.n_max, xs, cfg.layout, args.cpu_seconds)
+        from paper_2504_07637_b200 import boys
+        xd = wl.xs[0][: 1 << 21]
+        xs = xd.cpu().numpy()
+        g = boys(cfg.n_max, xd, layout=cfg.layout).cpu().numpy()
+        v, cores, reps, ulp = cpu_port_rate(cfg.n_max, xs, cfg.layout, args.cpu_seconds, g)
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
                                 "sample": f"{reps} x 2^21 points of {cfg.name} "
-                                          f"(~{args.cpu_seconds:.0f} s), OpenMP all threads"}
+                                          f"(~{args.cpu_seconds:.0f} s), OpenMP all threads",
+                                "max_ulp_gpu_vs_port": ulp}
 
     # the other BASELINE configurations (same protocol, fewer steps)
     if not args.no_extras:
