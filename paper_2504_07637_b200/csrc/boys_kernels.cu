@@ -574,11 +574,11 @@ struct RaggedWarp {
 
 template <typename T> struct alignas(4 * sizeof(T)) ZcRow { T z, c, x_up, pad; };  // per order
 
-template <typename T, int NB, int EPL, int CPE>
+template <typename T, int NB, int EPL, int CPE, int WT = kThreads>
 struct RaggedSmem {
   SmemTable<T, NB + 1> st;           // rows 0..NB (the fast path's orders)
   ZcRow<T> zc[NB + 1];               // per-order scalars, one 16/32-byte line each
-  RaggedWarp<T, NB, EPL, CPE> w[kThreads / 32];
+  RaggedWarp<T, NB, EPL, CPE> w[WT / 32];
 };
 
 // Elements above x_up(n) (upward-ladder branch) join the queue in fp32, where
@@ -636,8 +636,8 @@ template <> struct Sentinel<float> {
   static __device__ __forceinline__ bool is(float v) { return __float_as_int(v) == 0x7fa0c0de; }
 };
 
-template <typename T, int NB, int EPL, int CPE, int MINB>
-__global__ void __launch_bounds__(kThreads, MINB)
+template <typename T, int NB, int EPL, int CPE, int MINB, int WT = kThreads>
+__global__ void __launch_bounds__(WT, MINB)
 ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
               const int64_t* __restrict__ OFF, int64_t N, T* __restrict__ out,
               int64_t* __restrict__ dom) {
@@ -645,7 +645,8 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
   using WarpT = RaggedWarp<T, NB, EPL, CPE>;
   constexpr int CH = 32 * EPL;                   // elements per chunk
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  RaggedSmem<T, NB, EPL, CPE>& S = *reinterpret_cast<RaggedSmem<T, NB, EPL, CPE>*>(smem_raw);
+  using SmemT = RaggedSmem<T, NB, EPL, CPE, WT>;
+  SmemT& S = *reinterpret_cast<SmemT*>(smem_raw);
   stage_table(S.st);
   for (int k = threadIdx.x; k <= NB; k += blockDim.x)
     S.zc[k] = ZcRow<T>{Tab<T>::row(k).z, Tab<T>::row(k).c, Tab<T>::row(k).x_up, T(0)};
@@ -654,9 +655,9 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   WarpT& W = S.w[wid];
   const int64_t nchunks = (N + CH - 1) / CH;
-  const int64_t wstride = (int64_t)gridDim.x * (kThreads / 32);
+  const int64_t wstride = (int64_t)gridDim.x * (WT / 32);
   int qn = 0;                                    // warp-uniform queue length
-  int64_t c = (int64_t)blockIdx.x * (kThreads / 32) + wid;
+  int64_t c = (int64_t)blockIdx.x * (WT / 32) + wid;
   // software pipeline: inputs of chunk c are loaded one iteration ahead
   T px[EPL];
   int pn[EPL];
@@ -1272,14 +1273,14 @@ static boys_status opt_in_smem(K kernel, int smem, std::atomic<uint64_t>& mask) 
 // The occupancy query is cached per (kernel, shared-memory size): it is a
 // host-side call that would otherwise sit on every launch's critical path.
 template <typename K>
-static int blocks_for(K kernel, size_t smem, int64_t ntiles) {
+static int blocks_for(K kernel, size_t smem, int64_t ntiles, int threads = kThreads) {
   static thread_local struct { const void* k; size_t smem; int occ; } cache[8] = {};
   const void* key = reinterpret_cast<const void*>(kernel);
   int occ = 0;
   for (auto& c : cache)
     if (c.k == key && c.smem == smem) { occ = c.occ; break; }
   if (!occ) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, smem);
     if (occ < 1) occ = 1;
     for (auto& c : cache)
       if (!c.k) { c = {key, smem, occ}; break; }
@@ -1528,20 +1529,20 @@ static int ragged_epl() {   // BOYS_RAGGED_EPL=1: one element per lane (A/B)
   return v;
 }
 
-template <typename T, int NB, int EPL, int CPE, int MINB>
+template <typename T, int NB, int EPL, int CPE, int MINB, int WT = kThreads>
 static boys_status launch_chunks(const void* x, const uint8_t* nm, const int64_t* off, int64_t N,
                                  void* out, int64_t* dom, cudaStream_t s) {
-  auto k = ragged_kernel<T, NB, EPL, CPE, MINB>;
-  const size_t smem = sizeof(RaggedSmem<T, NB, EPL, CPE>);
+  auto k = ragged_kernel<T, NB, EPL, CPE, MINB, WT>;
+  const size_t smem = sizeof(RaggedSmem<T, NB, EPL, CPE, WT>);
   static std::atomic<uint64_t> attr_mask{0};
   boys_status st = opt_in_smem(k, (int)smem, attr_mask);
   if (st != BOYS_OK) return st;
   const int64_t nch = (N + 32 * EPL - 1) / (32 * EPL);
-  const int64_t nblk = (nch + 7) / 8;
-  int64_t grid = blocks_for(k, smem, nblk);
+  const int64_t nblk = (nch + WT / 32 - 1) / (WT / 32);
+  int64_t grid = blocks_for(k, smem, nblk, WT);
   grid *= ragged_grid_mult(sizeof(T) == 8);
   if (grid > nblk) grid = nblk;
-  k<<<(int)grid, kThreads, smem, s>>>((const T*)x, nm, off, N, (T*)out, dom);
+  k<<<(int)grid, WT, smem, s>>>((const T*)x, nm, off, N, (T*)out, dom);
   return BOYS_OK;
 }
 
@@ -1565,6 +1566,9 @@ static boys_status launch_ragged(const void* x, const uint8_t* nm, const int64_t
     // bound, measured no better: 1.96 / 2.08 ms f64)
     // (f64, 2 elements per lane with 10 staged values each, 24 warps/SM:
     // 1.88 ms -- within 1%, but overflows to the slow path from order 10)
+    // (128-thread blocks, also with a 96-register bound and 8 staged values per
+    // element for 20 resident warps, measured slower: f64 1.84-2.36 vs 1.78 ms,
+    // f32 0.94-1.00 vs 0.94 ms, tools/ab/ab39.sh)
     boys_status st = ragged_epl() == 1
                          ? launch_chunks<T, NB, 1, NB + 1, 0>(x, nm, off, N, out, dom, s)
                          : launch_chunks<T, NB, EPL, 12, 0>(x, nm, off, N, out, dom, s);
