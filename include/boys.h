@@ -20,6 +20,7 @@
  *       SPEC.md:302, 320, 347; refmath.py:111-115
  *   order check (refmath.py:104-108, MAX_ORDER :41)       BOYS_E_ORDER / boys_max_order
  *   eval_batch with host arrays (the CPU caller's view)   boys_eval_dense_host
+ *   ragged work lists with host arrays                   boys_eval_ragged_host
  *
  * Conventions
  *   - Device pointers are caller-owned, 16-byte aligned for x/out, and the work
