@@ -662,9 +662,11 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
   T px[EPL];
   int pn[EPL];
   int64_t poff[EPL], pbase = 0, plast_off = 0;
+  int prem = 0;                                  // elements of the prefetched chunk
   auto load = [&](int64_t cc) {
     const int64_t j0 = cc * CH;
     if (j0 + CH <= N) {                          // full chunk (warp-uniform): no predicates
+      prem = CH;
       const T* xp = X + j0 + lane;
       const uint8_t* np = NM + j0 + lane;
       const int64_t* op = OFF + j0 + lane;
@@ -677,6 +679,7 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
     } else {
       // elements of chunk cc that exist (warp-uniform, 0 past the end)
       const int rem = cc < nchunks ? (int)(N - j0) : 0;
+      prem = rem;
 #pragma unroll
       for (int e = 0; e < EPL; ++e) {
         const int64_t j = j0 + 32 * e + lane;
@@ -698,7 +701,7 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
     int n[EPL];
     int64_t goff[EPL];
     bool in[EPL];
-    const int rem = (int)((N - i0) < CH ? (N - i0) : CH);
+    const int rem = prem;
 #pragma unroll
     for (int e = 0; e < EPL; ++e) {
       x[e] = px[e];
