@@ -255,6 +255,21 @@ class Ragged:
         yield lambda: boys_ragged(self.x, self.nm, self.off, out=self.out, check=False)
 
 
+class Split(Dense):
+    """eval_with_split(16, 8) on the cfg3 inputs, point-major [N][17] (the
+    SPEC's two-seed accuracy option; same bytes per point as cfg3)."""
+
+    def __init__(self, rank, ws, dev):
+        from paper_2504_07637_b200 import workloads as W
+        super().__init__(W.CONFIGS["cfg3"], rank, ws, dev)
+        self.n_bar = 8
+
+    def launches(self):
+        from paper_2504_07637_b200 import eval_with_split
+        x, out = self.xs[0], self.outs[0]
+        yield lambda: eval_with_split(self.n, self.n_bar, x, layout="aos", check=False, out=out)
+
+
 def make_workload(name, rank, ws, dev, n_points=None, rotate=1):
     from paper_2504_07637_b200 import workloads as W
     cfg = W.CONFIGS[name]
@@ -587,12 +602,13 @@ def main():
         # launch (also evicts code and __constant__ tables: includes the cold
         # fetch latency of an isolated launch)
         plan = [("cfg1", "cfg1", 32, "graph"), ("cfg1_l2flush", "cfg1", 1, "flush")]
-        plan += [(n, n, 1, None) for n in ("cfg2", "cfg4", "cfg4f32", "cfg5")]
+        plan += [(n, n, 1, None) for n in ("cfg2", "cfg4", "cfg4f32", "cfg5", "split")]
         for key, name, rot, fl in plan:
             if name == args.config:
                 continue
             try:
-                w2 = make_workload(name, rank, ws, dev, rotate=rot)
+                w2 = (Split(rank, ws, dev) if name == "split"
+                      else make_workload(name, rank, ws, dev, rotate=rot))
                 k = min(args.steps, 50) if name != "cfg1" else (100 if rot > 1 else 200)
                 s2, p2, _, l2 = time_workload(
                     w2, k, args.warmup, ws, local,
@@ -608,6 +624,9 @@ def main():
                             "working set > L2)")
                 else:
                     note = "exceeds L2"
+                if name == "split":
+                    note = ("eval_with_split(16, 8) on the cfg3 inputs, AoS [N][17]; "
+                            "exceeds L2")
                 extras[key] = {"value": v2, "unit": UNIT, "steps": k,
                                "ms_per_step": s2 / k * 1e3, "scaling": w2.scaling,
                                "gpu_launches": l2,

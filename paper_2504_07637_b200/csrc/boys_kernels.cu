@@ -521,6 +521,62 @@ __device__ __forceinline__ void tail_rt(T x, T y, T t, int n, bool ok, int wmax,
   }
 }
 
+// Root-factored product with a warp-uniform run-time factor count: the
+// active steps of factored_rt (same products, same order), skipping the
+// inactive ones with a uniform branch instead of selecting them away.
+template <typename T, int MQ, int ML>
+__device__ __forceinline__ T factored_uniform(T x, const T (*q)[2], const T* l, int nq, int nl) {
+  using A = Ar<T>;
+  T acc = T(1);
+  bool first = true;
+#pragma unroll
+  for (int k = 0; k < MQ; ++k) {
+    if (k >= nq) break;
+    T d = A::sub(x, q[k][0]);
+    T f = A::fma(d, d, q[k][1]);
+    acc = first ? f : A::mul(acc, f);
+    first = false;
+  }
+#pragma unroll
+  for (int k = 0; k < ML; ++k) {
+    if (k >= nl) break;
+    T f = A::sub(x, l[k]);
+    acc = first ? f : A::mul(acc, f);
+    first = false;
+  }
+  return acc;
+}
+
+// eval_point_rt for an order that is the same on every lane of the warp
+// (split kernel): uniform loop bounds instead of per-lane selects.  Invalid
+// lanes evaluate x = 0 at that order and output NaN, as in eval_point_rt.
+template <typename T, int NB, typename Rows, typename Put>
+__device__ __forceinline__ void eval_point_uniform(T x_in, bool ok, int n, const Rows& rows,
+                                                   Put&& put) {
+  using A = Ar<T>;
+  constexpr int MQ = MaxShape<T>::Q(), ML = MaxShape<T>::L();
+  T x = ok ? x_in : T(0);
+  T t = exp_neg_clamped(x);
+  const BoysRow<T>& R = rows(n);
+  bool below = ok && x < R.z;
+  T y = x;
+  if (__any_sync(kFull, below)) {
+    T u = factored_uniform<T, MQ, ML>(x, R.uq, R.ul, R.cnt[0], R.cnt[1]);
+    T v = factored_uniform<T, MQ, ML>(x, R.vq, R.vl, R.cnt[2], R.cnt[3]);
+    T w = A::div(u, v);
+    T h = A::mul(R.q2, w);
+    h = A::fma(h, x, R.q1);
+    T Q = A::fma(h, x, R.q0);
+    T sq = A::sqrt(Q);
+    T s = n == 0 ? sq : A::mul(powi_rt_bounded(Q, n, 32 - __clz(n | 1)), sq);
+    T yq = A::fma(s, t, x);
+    y = below ? yq : x;
+  }
+  tail_rt<T, NB>(x, y, t, n, ok, n, rows, [&](int m, T v, bool on) {
+    if (on) put(m, v);
+  });
+}
+
 // Complete run-time-order evaluation (split kernel; ragged fallback tiles).
 template <typename T, int NB, typename Rows, typename Put>
 __device__ __forceinline__ void eval_point_rt(T x_in, bool ok, int n, const Rows& rows,
@@ -1157,28 +1213,56 @@ ragged_win_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
 // split kernel (eval_with_split): F_m for m <= nbar equals a
 // dense order-nbar evaluation, F_m for m > nbar a dense order-n evaluation.
 // ---------------------------------------------------------------------------
-template <typename T, int n, bool AOS>
-__global__ void __launch_bounds__(kThreads)
+template <typename T, int n, bool AOS, int NBUF>
+__global__ void __launch_bounds__(kThreads, AOS ? 4 : 1)
 split_kernel(const T* __restrict__ X, int64_t N, int nbar, T* __restrict__ out,
-             int64_t* __restrict__ dom) {
+             int64_t* __restrict__ dom, bool bulk_ok) {
   constexpr int W = n + 1;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < N; i0 += stride) {
-    const int64_t i = i0 + threadIdx.x;
+  constexpr int TILE_ELEMS = kThreads * W;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  T* sbase = reinterpret_cast<T*>(smem_raw);
+  const int tid = threadIdx.x;
+  const int64_t ntiles = (N + kThreads - 1) / kThreads;
+  pdl_wait_and_release();
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const int64_t i0 = tile * kThreads;
+    const int64_t i = i0 + tid;
     const bool in = i < N;
-    T x = in ? ldg_nc(X + i) : T(0);
+    const T x = in ? ldg_nc(X + i) : T(0);
     bool ok = valid_x(x);
     if (in && !ok) flag_domain(dom, i);
     ok = ok || !in;
-    T* o = AOS ? out + i * W : out + i;
-    const int64_t stride_m = AOS ? 1 : N;
-    eval_point_stream<T, n>(x, ok, [&](int m, T v) {
-      if (in && m > nbar) __stcs(o + m * stride_m, v);
-    });
-    eval_point_rt<T, n>(x, ok, nbar, ConstRows<T>{}, [&](int m, T v) {
-      if (in && m <= nbar) __stcs(o + m * stride_m, v);
-    });
+    if constexpr (AOS) {
+      // as the dense AoS path: [256][n+1] tile staged in shared memory (odd
+      // row stride: conflict-free), one bulk copy per tile, NBUF-deep
+      T* buf = sbase + (it % NBUF) * TILE_ELEMS;
+      if (tid == 0) bulk_wait_read<NBUF - 1>();
+      __syncthreads();
+      T* row = buf + tid * W;
+      eval_point_stream<T, n>(x, ok, [&](int m, T v) { if (m > nbar) row[m] = v; });
+      eval_point_uniform<T, n>(x, ok, nbar, ConstRows<T>{}, [&](int m, T v) { if (m <= nbar) row[m] = v; });
+      const int64_t cnt = (N - i0) < kThreads ? (N - i0) : kThreads;
+      if (bulk_ok && cnt == kThreads) {
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (tid == 0) bulk_store(out + i0 * W, buf, TILE_ELEMS * sizeof(T));
+      } else {
+        __syncthreads();
+        T* dst = out + i0 * W;
+        for (int k = tid; k < cnt * W; k += kThreads) __stcs(dst + k, buf[k]);
+      }
+    } else {
+      T* o = out + i;
+      eval_point_stream<T, n>(x, ok, [&](int m, T v) {
+        if (in && m > nbar) __stcs(o + (int64_t)m * N, v);
+      });
+      eval_point_uniform<T, n>(x, ok, nbar, ConstRows<T>{}, [&](int m, T v) {
+        if (in && m <= nbar) __stcs(o + (int64_t)m * N, v);
+      });
+    }
   }
+  if (AOS && tid == 0) bulk_wait_all();
 }
 
 // ---------------------------------------------------------------------------
@@ -1477,9 +1561,18 @@ static boys_status eval_dense_base(boys_dtype dtype, int n_max, const void* x, i
 template <typename T, int n, bool AOS>
 static boys_status launch_split_t(const T* x, int64_t N, int nbar, T* out, int64_t* dom,
                                   cudaStream_t s) {
-  auto k = split_kernel<T, n, AOS>;
-  int64_t ntiles = (N + kThreads - 1) / kThreads;
-  k<<<blocks_for(k, 0, ntiles), kThreads, 0, s>>>(x, N, nbar, out, dom);
+  constexpr bool fits2 = 2 * kThreads * (n + 1) * sizeof(T) <= 80 * 1024;
+  constexpr int NBUF = (AOS && fits2) ? 2 : 1;
+  auto k = split_kernel<T, n, AOS, NBUF>;
+  const size_t smem = AOS ? (size_t)NBUF * kThreads * (n + 1) * sizeof(T) : 0;
+  static std::atomic<uint64_t> attr_mask{0};
+  if (AOS) {
+    boys_status st = opt_in_smem(k, (int)smem, attr_mask);
+    if (st != BOYS_OK) return st;
+  }
+  const int64_t ntiles = (N + kThreads - 1) / kThreads;
+  const bool bulk_ok = (reinterpret_cast<uintptr_t>(out) % 16) == 0;
+  k<<<blocks_for(k, smem, ntiles), kThreads, smem, s>>>(x, N, nbar, out, dom, bulk_ok);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cuda_status(cudaGetLastError());
 }

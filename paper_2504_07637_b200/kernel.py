@@ -199,9 +199,10 @@ def eval_fn(n: int, x, table=None):
     return fn, ex
 
 
-def eval_with_split(n: int, n_bar: int, x, layout: str = "soa", check: bool = True):
+def eval_with_split(n: int, n_bar: int, x, layout: str = "soa", check: bool = True, out=None):
     """F_{n_bar+1..n} from the order-n seed, F_{0..n_bar} from
-    the order-n_bar seed (two recursions)."""
+    the order-n_bar seed (two recursions).  ``out``: optional preallocated
+    device tensor of the result's shape (device inputs only)."""
     xt = x if isinstance(x, torch.Tensor) and x.is_cuda else torch.as_tensor(
         np.asarray(x)).cuda()
     _check_order(n, xt.dtype)
@@ -210,8 +211,12 @@ def eval_with_split(n: int, n_bar: int, x, layout: str = "soa", check: bool = Tr
     lay = _layout(layout)
     xf = _as_device_x(xt)
     N = xf.numel()
-    out = torch.empty((n + 1, N) if lay == L.BOYS_SOA else (N, n + 1), dtype=xt.dtype,
-                      device=xt.device)
+    shape = (n + 1, N) if lay == L.BOYS_SOA else (N, n + 1)
+    if out is None:
+        out = torch.empty(shape, dtype=xt.dtype, device=xt.device)
+    elif (tuple(out.shape) != shape or out.dtype != xt.dtype or out.device != xt.device
+          or not out.is_contiguous()):
+        raise ValueError(f"out must be a contiguous {xt.dtype} tensor of shape {shape}")
     dom = torch.full((1,), -1, dtype=torch.int64, device=xt.device) if check else None
     with torch.cuda.device(xt.device):
         L.check(L.load().boys_eval_split(_DTYPES[xt.dtype], n, n_bar, _ptr(xf), N, _ptr(out), lay,

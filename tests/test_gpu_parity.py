@@ -227,6 +227,12 @@ def test_split_bit_exact(oracle, dtype):
             got = eval_with_split(n, nbar, torch.from_numpy(x).cuda(), layout=layout)
             ref, bad = oracle.split(n, nbar, x, layout)
             assert_parity(got.cpu().numpy(), ref, f"split {n}/{nbar} {layout}")
+    # many tiles per block (persistent loop, double-buffered AoS staging) + a tail
+    xl = dense_inputs(dtype, 16, N=(1 << 20) + 5)
+    for layout in ("aos", "soa"):
+        got = eval_with_split(16, 8, torch.from_numpy(xl).cuda(), layout=layout)
+        ref, _ = oracle.split(16, 8, xl, layout)
+        assert_parity(got.cpu().numpy(), ref, f"split 16/8 {layout} 2^20+5")
     # n_bar = n-1: low segment identical to a direct eval at n_bar
     lo = boys(mx - 1, torch.from_numpy(x).cuda()).cpu().numpy()
     sp = eval_with_split(mx, mx - 1, torch.from_numpy(x).cuda()).cpu().numpy()
