@@ -40,6 +40,9 @@ constexpr int kRaggedFastOrders = 16;
 #define BOYS_SOA_MINB 4   // SoA resident-block target (register budget 64/thread)
 #endif
 constexpr unsigned kFull = 0xffffffffu;
+#ifndef BOYS_PAIR_MINB_SMALL
+#define BOYS_PAIR_MINB_SMALL 5   // paired SoA kernel, n <= 1: resident-block target (47 registers; cfg1 9.27 us vs 9.50 / 9.71 / 9.65 / 9.75 for 6 / 4 / 3 / 8)
+#endif
 #ifndef BOYS_PAIR_FASTCR
 #define BOYS_PAIR_FASTCR 0   // 1: paired SoA kernel shares fast-path checks for div/sqrt/rcp (A/B: slower, spills: cfg1 10.7 vs 9.5 us)
 #endif
@@ -1485,7 +1488,7 @@ static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 
 template <typename T, int n>
 static boys_status launch_soa_pair(const T* x, int64_t N, T* out, T* expx, int64_t* dom,
                                    int64_t base, cudaStream_t s) {
-  constexpr int MINB = n <= 1 ? 6 : BOYS_SOA_MINB;   // two chains: 8 blocks would spill at n = 0
+  constexpr int MINB = n <= 1 ? BOYS_PAIR_MINB_SMALL : BOYS_SOA_MINB;   // two chains: 8 blocks would spill at n = 0
   auto k = dense_soa_pair_kernel<T, n, MINB>;
   const int64_t ntiles = (N + 2 * kThreads - 1) / (2 * kThreads);
   int grid = blocks_for(k, 0, ntiles);
