@@ -93,3 +93,19 @@ def test_oracle_library_exports():
     for s in ("boys_oracle_load", "boys_oracle_dense", "boys_oracle_ragged", "boys_oracle_split",
               "boys_oracle_qtilde", "boys_oracle_expneg"):
         assert hasattr(L, s)
+
+
+def test_c_example_compiles_and_links(tmp_path):
+    """include/boys.h is plain C and libboys.so links from a C host
+    (examples/c_host.c; the GPU test runs it)."""
+    import shutil
+    import subprocess
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc absent")
+    from paper_2504_07637_b200 import build as B
+    exe = tmp_path / "c_host"
+    subprocess.run(["gcc", "-O2", "-std=c11", "-Wall", "-Werror", "-I", str(ROOT / "include"),
+                    str(ROOT / "examples" / "c_host.c"), "-L", str(B.PKG), "-lboys",
+                    f"-Wl,-rpath,{B.PKG}", "-o", str(exe)], check=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert r.returncode == 64 and "usage" in r.stderr
