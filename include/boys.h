@@ -60,7 +60,7 @@ typedef enum {
 typedef enum { BOYS_F64 = 0, BOYS_F32 = 1 } boys_dtype;
 typedef enum { BOYS_SOA = 0, BOYS_AOS = 1 } boys_layout;
 
-/* Highest tabulated order for the dtype (16 for f64, 8 for f32). */
+/* Highest tabulated order for the dtype (36 for f64, 16 for f32). */
 int boys_max_order(boys_dtype dtype);
 
 /* Library / table version string ("libboys <ver> tables <sha-prefix>"). */
