@@ -67,7 +67,7 @@ int boys_max_order(boys_dtype dtype);
 const char* boys_version(void);
 
 /* F_0..F_{n_max}(x_i) for i < N into out_dev (layout as above).
- * expx_dev (nullable): e^{-x_i} as used by the recursion (0 for x > 708 / 87). */
+ * expx_dev (nullable): e^{-x_i} as used by the recursion (0 for x > 708 in f64, x > 86 in f32). */
 boys_status boys_eval_dense(boys_dtype dtype, int n_max, const void* x_dev, int64_t N,
                             void* out_dev, boys_layout layout, void* expx_dev,
                             int64_t* dom_dev, void* stream);
