@@ -1,19 +1,25 @@
 // sm_100a kernels and the C ABI of libboys (include/boys.h).
 //
-// dense  : persistent grid of 256-point tiles, one point per thread; each
-//          F_m is streamed to its destination as the recursion produces it
-//          (no per-thread value array).
-//          SoA -> coalesced streaming stores, one row per order.
-//          AoS -> the [256][n+1] tile is staged in shared memory (odd row
-//                 stride => conflict-free 64-bit banks) and leaves as ONE bulk
-//                 async copy (cp.async.bulk.global.shared::cta, TMA engine)
-//                 that overlaps the next tile's computation.
-// ragged : per-element order.  Per tile: ballot-compact the elements needing
-//          e^{-x} (x <= XEXP) and Q~ (x < z_{n_i}) into one work list (phase
-//          A); then every lane runs the cheap run-time-order tail for its own
-//          element, recursion bounded by the warp's largest order (phase B);
-//          output staged per tile, written with coalesced stores.
-// split  : eval_with_split (two seeds, two recursions).
+// dense  : each F_m is streamed to its destination as the recursion produces
+//          it (no per-thread value array); launches use programmatic
+//          dependent launch (griddepcontrol) to overlap back-to-back kernels.
+//          SoA  -> paired kernel: two adjacent points per thread, 16-byte x
+//                  loads and 16-byte streaming stores per F_m row, one block
+//                  per 512-point tile (one point per thread for odd N /
+//                  unaligned buffers).
+//          AoS  -> persistent grid of 256-point tiles; the [256][n+1] tile is
+//                  staged in shared memory (odd row stride => conflict-free
+//                  64-bit banks) and leaves as ONE bulk async copy
+//                  (cp.async.bulk.global.shared::cta, TMA engine) that
+//                  overlaps the next tile's computation.
+// ragged : per-element order.  Warp-autonomous chunks of 32*EPL elements:
+//          past-cut-off elements run the run-time-order tail into a staging
+//          slot (jump-table entry into the unrolled recursion), below-cut-off
+//          ones go to a warp queue evaluated 32 at a time; each chunk's output
+//          range leaves as one bulk async copy.
+// split  : eval_with_split (two seeds, two recursions), AoS staged as dense.
+// host   : host-buffer pipelines (H2D / kernel / D2H over chunks, two streams)
+//          for dense and ragged work.
 // All values are bit-identical to the CPU oracle (oracle/boys_oracle.c).
 #include <cuda_runtime.h>
 
@@ -966,251 +972,10 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
   if (lane == 0) bulk_wait_all();
 }
 
-// ---------------------------------------------------------------------------
-// ragged kernel, block windows (v9): 1024 consecutive elements per window.
-//   P0  load + classify: bucket = order n for elements past their cut-off,
-//       kDeferB for elements below it (Q~ needed), skip for padding;
-//       histogram with warp-aggregated shared atomics (rank within bucket)
-//   P1  scan (warp 0); tasks of <= 32 elements never straddling a bucket
-//   P2  scatter element slots into bucket order
-//   P3  warps take tasks: one compile-time-order tail per task (switch jump
-//       table, no per-lane divergence); the below-cut-off bucket runs the
-//       run-time-order path; values staged at their output offsets
-//   P4  the window's contiguous output range leaves as one bulk copy
-// Windows holding an order above NB, or whose output exceeds the staging
-// capacity, are evaluated per element with direct writes.
-// Values are bit-identical to boys_eval_dense at each element's order.
-// ---------------------------------------------------------------------------
-constexpr int kWinPer = 4;                       // elements per thread per window
-
-template <typename T, int NB, int WT>
-struct RaggedWinSmem {
-  static constexpr int kWin = WT * kWinPer;
-  // bucket ids: 0 = below the cut-off (expensive: first in the task list so
-  // the static striping starts warps 0.. on them), 1 + n = past-cut-off
-  // elements of order n, NB + 2 = padding (no tasks)
-  static constexpr int kDeferB = 0, kSkipB = NB + 2, kBuckets = NB + 3;
-  static constexpr int CAP = kWin * 6;           // staged values (ERI-like mean: ~4.1 per element)
-  static constexpr int MAXTASKS = (WT * kWinPer) / 32 + kBuckets;
-  SmemTable<T, NB + 1> st;
-  alignas(16) T stage[CAP + 16 / sizeof(T)];
-  T ex[kWin];
-  int eloc[kWin];
-  unsigned char en[kWin];
-  short perm[kWin];
-  int hist[kBuckets];
-  int tstart[MAXTASKS];
-  unsigned char tbucket[MAXTASKS], tcount[MAXTASKS];
-  int ntasks, any_hi;
-};
-
-// compile-time-order tail of a past-cut-off element (y = x) into dst[0..n]
-template <typename T, int n>
-__device__ __forceinline__ void win_tail(T x, bool on, T* dst) {
-  using A = Ar<T>;
-  const BoysRow<T>& R = Tab<T>::row(n);
-  const T t = exp_neg_clamped(x);
-  const T r = A::rcp(x);
-  const T sr = A::sqrt(r);
-  T cur = n == 0 ? A::mul(R.c, sr) : A::mul(A::mul(R.c, powi<T, (n == 0 ? 1 : n)>(r)), sr);
-  if (on) dst[n] = cur;
-  const T tx = A::add(x, x);
-#pragma unroll
-  for (int m = n - 1; m >= 0; --m) {
-    cur = A::mul(A::fma(tx, cur, t), rinv<T>(m));
-    if (on) dst[m] = cur;
-  }
-  const bool up = on && x > R.x_up;
-  if (__any_sync(kFull, up)) {
-    const T rx = A::rcp(x);
-    T f = up_first(x);
-    if (up) dst[0] = f;
-#pragma unroll
-    for (int m = 0; m < n; ++m) {
-      f = up_next(f, m, rx);
-      if (up) dst[m + 1] = f;
-    }
-  }
-}
-
-template <typename T, int NB, int n = 0>
-__device__ __forceinline__ void win_dispatch(int b, T x, bool on, T* dst) {
-  if constexpr (n <= NB) {
-    if (b == n) win_tail<T, n>(x, on, dst);
-    else win_dispatch<T, NB, n + 1>(b, x, on, dst);
-  }
-}
-
-template <typename T, int NB, int WT>
-__global__ void __launch_bounds__(WT, (WT == 128 ? 6 : WT == 256 ? 3 : 1))
-ragged_win_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
-                  const int64_t* __restrict__ OFF, int64_t N, T* __restrict__ out,
-                  int64_t* __restrict__ dom) {
-  using A = Ar<T>;
-  using SM = RaggedWinSmem<T, NB, WT>;
-  constexpr int kWin = SM::kWin;
-  constexpr int Q = 16 / sizeof(T), MAXN = Tab<T>::MAX_ORDER;
-  constexpr int kDeferB = SM::kDeferB, kSkipB = SM::kSkipB, kBuckets = SM::kBuckets;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  SM& S = *reinterpret_cast<SM*>(smem_raw);
-  stage_table(S.st);
-  const SmemRows<T> rows{S.st.row};
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const unsigned lt = (1u << lane) - 1u;
-  const int64_t nwin = (N + kWin - 1) / kWin;
-  // software pipeline: the next window's inputs are loaded into registers
-  // while the current window runs P1..P4
-  T px[kWinPer];
-  int pn[kWinPer];
-  int64_t poff[kWinPer], pbase = 0, plast = 0;
-  auto load = [&](int64_t ww) {
-    if (ww >= nwin) return;
-    const int64_t a0 = ww * kWin;
-    const int64_t al = (a0 + kWin < N) ? a0 + kWin : N;
-    pbase = __ldg(OFF + a0);
-    plast = __ldg(OFF + al);
-#pragma unroll
-    for (int k = 0; k < kWinPer; ++k) {
-      const int64_t i = a0 + k * WT + tid;
-      const bool in = i < N;
-      px[k] = in ? ldg_nc(X + i) : T(0);
-      pn[k] = in ? (int)NM[i] : 0;
-      poff[k] = in ? __ldg(OFF + i) : 0;
-    }
-  };
-  load(blockIdx.x);
-  for (int64_t w = blockIdx.x; w < nwin; w += gridDim.x) {
-    const int64_t w0 = w * kWin;
-    const int64_t base = pbase;
-    const int64_t cnt = plast - pbase;
-    if (tid < kBuckets) S.hist[tid] = 0;
-    if (tid == 0) S.any_hi = 0;
-    __syncthreads();                                         // (0) previous window done
-    // ---- P0: classify, rank within bucket ---------------------------------
-    int rank[kWinPer], key[kWinPer];
-    bool hi = false;
-#pragma unroll
-    for (int k = 0; k < kWinPer; ++k) {
-      const int slot = k * WT + tid;                   // coalesced
-      const int64_t i = w0 + slot;
-      const bool in = i < N;
-      const T x = px[k];
-      const int n = pn[k];
-      const bool xok = valid_x(x);
-      if (in && !(xok && n <= MAXN)) flag_domain(dom, i);
-      hi = hi || (in && n > NB);
-      const int nn = n <= NB ? n : 0;
-      const T xs = (in && xok) ? x : A::nan();
-      int b = kSkipB;
-      if (in && n <= NB) b = (xok && xs < rows(nn).z) ? kDeferB : nn + 1;
-      S.ex[slot] = xs;
-      S.en[slot] = (unsigned char)nn;
-      S.eloc[slot] = in ? (int)(poff[k] - base) + (int)(base & (Q - 1)) : 0;
-      const unsigned peers = __match_any_sync(kFull, b);
-      const int leader = __ffs(peers) - 1;
-      int b0 = 0;
-      if (lane == leader) b0 = atomicAdd(&S.hist[b], __popc(peers));
-      rank[k] = __shfl_sync(kFull, b0, leader) + __popc(peers & lt);
-      key[k] = b;
-    }
-    if (hi) S.any_hi = 1;
-    load(w + gridDim.x);                                     // prefetch the next window
-    if (tid == 0) bulk_wait_read<0>();                       // staging free again
-    __syncthreads();                                         // (1)
-    const bool per_elem = S.any_hi || cnt + Q > SM::CAP;
-    if (per_elem) {
-      // an order above NB or an oversized window: per-element direct writes
-#pragma unroll
-      for (int k = 0; k < kWinPer; ++k) {
-        const int slot = k * WT + tid;
-        const int64_t i = w0 + slot;
-        const bool in = i < N;
-        const T x = in ? ldg_nc(X + i) : T(0);
-        const int n = in ? (int)NM[i] : 0;
-        const int64_t goff = in ? __ldg(OFF + i) : 0;
-        if (in && n > MAXN) {
-          for (int m = 0; m <= n; ++m) out[goff + m] = A::nan();
-        }
-        const bool okl = in && valid_x(x) && n <= MAXN;
-        T* dst = out + goff;
-        const bool wr = in && n <= MAXN;
-        eval_point_rt<T, MAXN>(x, okl, okl ? n : 0, ConstRows<T>{},
-                               [&](int m, T v) { if (wr) dst[m] = v; });
-      }
-      continue;
-    }
-    // ---- P1: scan + task list (warp 0) ------------------------------------
-    if (warp == 0) {
-      const int h = lane < kBuckets ? S.hist[lane] : 0;
-      int v = h;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const int o = __shfl_up_sync(kFull, v, d);
-        if (lane >= d) v += o;
-      }
-      const int start = v - h;
-      const int nt = (lane < kSkipB) ? (h + 31) / 32 : 0;   // skip bucket has no tasks
-      int tv = nt;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const int o = __shfl_up_sync(kFull, tv, d);
-        if (lane >= d) tv += o;
-      }
-      const int t0 = tv - nt;
-      for (int j = 0; j < nt; ++j) {
-        S.tstart[t0 + j] = start + 32 * j;
-        S.tbucket[t0 + j] = (unsigned char)lane;
-        S.tcount[t0 + j] = (unsigned char)min(32, h - 32 * j);
-      }
-      if (lane == 31) S.ntasks = tv;
-      if (lane < kBuckets) S.hist[lane] = start;
-    }
-    __syncthreads();                                         // (2)
-    // ---- P2: scatter slots into bucket order --------------------------------
-#pragma unroll
-    for (int k = 0; k < kWinPer; ++k)
-      if (key[k] != kSkipB) S.perm[S.hist[key[k]] + rank[k]] = (short)(k * WT + tid);
-    __syncthreads();                                         // (3)
-    // ---- P3: tasks ------------------------------------------------------------
-    const int ntasks = S.ntasks;
-    for (int tk = warp; tk < ntasks; tk += WT / 32) {
-      const int b = S.tbucket[tk];
-      const bool has = lane < S.tcount[tk];
-      const int e = has ? S.perm[S.tstart[tk] + lane] : 0;
-      const T x = has ? S.ex[e] : T(0);
-      T* dst = S.stage + (has ? S.eloc[e] : 0);
-      if (b == kDeferB) {
-        const int n = has ? (int)S.en[e] : 0;
-        const T xe = has ? x : T(0);
-        const T t = exp_neg_clamped(xe);
-        const T y = has ? y_below_rt(xe, t, n, rows) : xe;
-        const int wmax = __reduce_max_sync(kFull, (unsigned)n);
-        T* sink = S.stage + SM::CAP + (lane & (Q - 1));     // beyond the staged range
-        tail_rt<T, NB>(xe, y, t, n, has, wmax, rows,
-                       [&](int m, T v, bool on) { *((has && on) ? dst + m : sink) = v; });
-      } else {
-        win_dispatch<T, NB>(b - 1, has ? x : T(1), has, dst);
-      }
-    }
-    __syncthreads();                                         // (4) staging complete
-    // ---- P4: one bulk copy of the window's output range -----------------------
-    if (warp == 0) {
-      const int shift = (int)(base & (Q - 1));
-      const int ncnt = (int)cnt;
-      const int head = ((Q - shift) & (Q - 1)) < ncnt ? ((Q - shift) & (Q - 1)) : ncnt;
-      const int body = ((ncnt - head) / Q) * Q;
-      const int tail0 = head + body;
-      if (lane < head) __stcs(out + base + lane, S.stage[shift + lane]);
-      if (lane < ncnt - tail0) __stcs(out + base + tail0 + lane, S.stage[shift + tail0 + lane]);
-      if (body > 0) {
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) bulk_store(out + base + head, S.stage + shift + head, body * sizeof(T));
-      }
-    }
-  }
-  if (tid == 0) bulk_wait_all();
-}
+// (A block-window ragged variant -- 1024-element windows counting-sorted into
+// order buckets, one compile-time-order tail per warp task -- measured slower
+// than the warp chunks for both dtypes (f64 2.59 vs 1.92 ms, f32 1.19 vs
+// 1.00 ms) and was removed; it is in the history up to commit 50d605b.)
 
 // ---------------------------------------------------------------------------
 // split kernel (eval_with_split): F_m for m <= nbar equals a
@@ -1594,35 +1359,6 @@ static boys_status dispatch_split(int nn, int nbar, const void* x, int64_t N, vo
   }
 }
 
-// Ragged kernel, chosen by same-box measurement on B200 (cfg4):
-//   f32: block windows 1.19 ms vs warp chunks 1.14 ms (4 elements per lane)
-//   f64: block windows 2.59 ms vs warp chunks 1.95 ms (3 elements per lane)
-// (f64's heavier below-cut-off tasks leave the window barriers waiting).
-// BOYS_RAGGED_WIN=1 selects the window kernel (A/B).
-template <typename T>
-static bool ragged_win() {
-  static int v = env_int("BOYS_RAGGED_WIN", -1);
-  return v == 1;          // default: warp chunks (faster for both dtypes)
-}
-
-template <typename T, int NB, int WT>
-static boys_status launch_win(const void* x, const uint8_t* nm, const int64_t* off, int64_t N,
-                              void* out, int64_t* dom, cudaStream_t s) {
-  auto k = ragged_win_kernel<T, NB, WT>;
-  const size_t smem = sizeof(RaggedWinSmem<T, NB, WT>);
-  static std::atomic<uint64_t> attr_mask{0};
-  boys_status st = opt_in_smem(k, (int)smem, attr_mask);
-  if (st != BOYS_OK) return st;
-  const int64_t win = (int64_t)WT * kWinPer;
-  const int64_t nwin = (N + win - 1) / win;
-  int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, WT, smem);
-  int64_t grid = (int64_t)sm_count() * (occ < 1 ? 1 : occ);
-  if (nwin < grid) grid = nwin;
-  k<<<(int)(grid < 1 ? 1 : grid), WT, smem, s>>>((const T*)x, nm, off, N, (T*)out, dom);
-  return cuda_status(cudaGetLastError());
-}
-
 static int ragged_epl() {   // BOYS_RAGGED_EPL=1: one element per lane (A/B)
   static int v = env_int("BOYS_RAGGED_EPL", 0);
   return v;
@@ -1651,12 +1387,7 @@ static boys_status launch_ragged(const void* x, const uint8_t* nm, const int64_t
   // fast-path order bound; higher orders, up to the table maximum, take the
   // in-kernel per-element fallback path
   constexpr int NB = Tab<T>::MAX_ORDER < kRaggedFastOrders ? Tab<T>::MAX_ORDER : kRaggedFastOrders;
-  if (ragged_win<T>()) {
-    // 256-thread blocks / 1024-element windows: measured best (f32 cfg4:
-    // 128 -> 1.27 ms, 256 -> 1.19 ms, 512 -> 2.04 ms)
-    boys_status st = launch_win<T, NB, 256>(x, nm, off, N, out, dom, s);
-    if (st != BOYS_OK) return st;
-  } else {
+  {
     // (order-sorted warp super-chunks were measured slower: 2.90 / 3.79 ms vs 2.42)
     // elements per lane: measured best 3 (f64: 1.95 ms vs 2.27 / 1.97 / 2.05
     // for 1 / 2 / 4) and 4 (f32: 1.14 ms vs 1.26 / 1.16 / 1.36 for 2 / 3 / 6)

@@ -21,7 +21,6 @@ KNOBS = [
     {"BOYS_AOS_NBUF": "1"},
     {"BOYS_AOS_NBUF": "1", "BOYS_AOS_MINB": "6"},
     {"BOYS_SOA0_MINB": "6", "BOYS_SOA_PAIR": "0"},
-    {"BOYS_RAGGED_WIN": "1"},
     {"BOYS_RAGGED_EPL": "1"},
     {"BOYS_RAGGED_GRID_MULT": "3"},
 ]
