@@ -11,15 +11,18 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libboys.so"
 PROBE_LIB = PKG / "libboys_probe.so"
-SOURCES = [CSRC / "boys_kernels.cu", CSRC / "boys_eval.cuh", CSRC / "boys_tables.inc",
-           PKG.parent / "include" / "boys.h"]
+# translation units of libboys (compiled in parallel, linked into one .so)
+UNITS = [CSRC / "dense.cu", CSRC / "ragged.cu", CSRC / "split.cu", CSRC / "abi.cu"]
+SOURCES = UNITS + [CSRC / "boys_device.cuh", CSRC / "boys_launch.h", CSRC / "boys_eval.cuh",
+                   CSRC / "boys_tables.inc", PKG.parent / "include" / "boys.h"]
 
-NVCC_FLAGS = [
+ARCH_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
     "-fmad=false",            # belt and braces: the evaluator uses explicit __*_rn intrinsics
-    "-Xcompiler", "-fPIC", "-shared",
+    "-Xcompiler", "-fPIC",
 ]
+NVCC_FLAGS = ARCH_FLAGS + ["-shared"]
 
 
 def nvcc() -> str:
@@ -39,7 +42,21 @@ def stale() -> bool:
 def build_libboys(force: bool = False, verbose: bool = False) -> Path:
     if not force and not stale():
         return LIB
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", str(LIB) + ".tmp", str(CSRC / "boys_kernels.cu")]
+    from concurrent.futures import ThreadPoolExecutor
+    objdir = PKG / "build"
+    objdir.mkdir(exist_ok=True)
+
+    def compile_unit(src: Path) -> Path:
+        obj = objdir / (src.stem + ".o")
+        cmd = [nvcc(), *ARCH_FLAGS, "-c", "-o", str(obj), str(src)]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.run(cmd, check=True)
+        return obj
+
+    with ThreadPoolExecutor(max_workers=len(UNITS)) as pool:
+        objs = list(pool.map(compile_unit, UNITS))
+    cmd = [nvcc(), *NVCC_FLAGS, "-o", str(LIB) + ".tmp", *map(str, objs)]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True)

@@ -1,0 +1,456 @@
+// Device-side building blocks shared by the libboys kernels: bulk-copy and
+// predication helpers, the compile-time-order evaluators (one point / two
+// points per thread) and the run-time-order evaluators (ragged / split).
+// All arithmetic follows boys_eval.cuh (bit-identical to the CPU oracle).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <type_traits>
+
+#include "../../include/boys.h"
+#include "boys_eval.cuh"
+
+namespace boys {
+
+constexpr int kThreads = 256;   // points per tile == threads per block
+constexpr int kRaggedFastOrders = 16;
+#ifndef BOYS_SOA_MINB
+#define BOYS_SOA_MINB 4   // SoA resident-block target (register budget 64/thread)
+#endif
+constexpr unsigned kFull = 0xffffffffu;
+#ifndef BOYS_PAIR_MINB_SMALL
+#define BOYS_PAIR_MINB_SMALL 5   // paired SoA kernel, n <= 1: resident-block target (47 registers; cfg1 9.27 us vs 9.50 / 9.71 / 9.65 / 9.75 for 6 / 4 / 3 / 8)
+#endif
+#ifndef BOYS_PAIR_FASTCR
+#define BOYS_PAIR_FASTCR 0   // 1: paired SoA kernel shares fast-path checks for div/sqrt/rcp (A/B: slower, spills: cfg1 10.7 vs 9.5 us)
+#endif
+#ifndef BOYS_FAST_CR
+#define BOYS_FAST_CR 0   // 1: ragged chunks use the branch-free CR rcp/sqrt fast paths (A/B: f64 1.88 vs 1.83 ms, slower)
+#endif
+
+
+__device__ __forceinline__ void flag_domain(int64_t* dom, int64_t i) {
+  if (dom) atomicMin(reinterpret_cast<unsigned long long*>(dom), (unsigned long long)i);
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// bulk async copy smem -> global (TMA engine); bytes % 16 == 0, both 16B aligned
+__device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(gdst),
+               "r"(smem_u32(ssrc)), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+}
+template <int PENDING>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;\n" ::"n"(PENDING) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+
+template <typename T> __device__ __forceinline__ T ldg_nc(const T* p) { return __ldg(p); }
+
+// Programmatic dependent launch (launches with the programmatic-serialization
+// attribute): wait until the stream's previous grid has completed and its
+// memory is visible (a no-op for a normally serialised launch), then allow
+// the stream's next grid to be scheduled onto SM slots as ours free up --
+// only its launch and prologue overlap our tail; it waits the same way.
+__device__ __forceinline__ void pdl_wait_and_release() {
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+
+// Predicated move / shared store (inline PTX so the compiler keeps plain
+// predication instead of a divergent branch per recursion step).
+__device__ __forceinline__ void pmov(bool p, double& dst, double v) {
+  asm("{ .reg .pred q; setp.ne.b32 q, %2, 0; @q mov.b64 %0, %1; }" : "+d"(dst) : "d"(v), "r"((int)p));
+}
+__device__ __forceinline__ void pmov(bool p, float& dst, float v) {
+  asm("{ .reg .pred q; setp.ne.b32 q, %2, 0; @q mov.b32 %0, %1; }" : "+f"(dst) : "f"(v), "r"((int)p));
+}
+__device__ __forceinline__ void psts(bool p, double* a, double v) {
+  asm volatile("{ .reg .pred q; setp.ne.b32 q, %2, 0; @q st.shared.f64 [%0], %1; }"
+               :: "r"(smem_u32(a)), "d"(v), "r"((int)p) : "memory");
+}
+__device__ __forceinline__ void psts(bool p, float* a, float v) {
+  asm volatile("{ .reg .pred q; setp.ne.b32 q, %2, 0; @q st.shared.f32 [%0], %1; }"
+               :: "r"(smem_u32(a)), "f"(v), "r"((int)p) : "memory");
+}
+
+
+
+// F_0..F_n for one point, handed to put(m, value) in the order n, n-1, .., 0
+// (then, for lanes past x_up, 0..n again with the upward values).  Returns
+// e^{-x}.  `ok` = x in the domain; other lanes produce NaN.  Lanes only
+// influence warp-uniform shortcuts (skip Q~ / the upward ladder), never values.
+template <typename T, int n, typename Put>
+__device__ __forceinline__ T eval_point_stream(T x_in, bool ok, Put&& put) {
+  using A = Ar<T>;
+  const BoysRow<T>& R = Tab<T>::row(n);
+  const T bad = A::nan();
+  // invalid lanes carry x = NaN: every IEEE step then yields NaN on its own
+  // (t = 0, y = r = F = NaN, the recursion stays NaN, the ladder test is
+  // false) -- no per-value select; valid lanes are untouched
+  T x = ok ? x_in : bad;
+  T t = exp_neg_clamped(x);
+  bool any_below = __any_sync(kFull, ok && x < R.z);
+  T cur = seed<T, n>(x, t, any_below);
+  put(n, cur);
+  T tx = A::add(x, x);
+#pragma unroll
+  for (int m = n - 1; m >= 0; --m) {
+    cur = A::mul(A::fma(tx, cur, t), rinv<T>(m));
+    put(m, cur);
+  }
+  bool up = ok && x > R.x_up;
+  if (__any_sync(kFull, up)) {
+    T rx = A::rcp(x);
+    T f = up_first(x);
+    if (up) put(0, f);
+#pragma unroll
+    for (int m = 0; m < n; ++m) {
+      f = up_next(f, m, rx);
+      if (up) put(m + 1, f);
+    }
+  }
+  return ok ? t : bad;
+}
+
+// Array form (split kernel).
+template <typename T, int n>
+__device__ __forceinline__ void eval_point(T x_in, bool ok, T (&Fv)[n + 1], T& t_out) {
+  t_out = eval_point_stream<T, n>(x_in, ok, [&](int m, T v) { Fv[m] = v; });
+}
+
+// seed<double, n> for two points with the correctly rounded div / sqrt / rcp
+// taken through their branch-free fast paths (boys_eval.cuh, bit-identical to
+// the intrinsics): one warp vote per operation decides whether any lane needs
+// the intrinsic instead, so the two chains share one check per operation.
+template <int n>
+__device__ __forceinline__ void seed_pair(const double (&x)[2], const double (&t)[2],
+                                          bool any_below, double (&F)[2]) {
+  using A = Ar<double>;
+  const BoysRow<double>& R = Tab<double>::row(n);
+  double y[2] = {x[0], x[1]};
+  if (any_below) {
+    constexpr int LU = Tab<double>::shape(n, 0), lu = Tab<double>::shape(n, 1);
+    constexpr int LV = Tab<double>::shape(n, 2), lv = Tab<double>::shape(n, 3);
+    double u[2], v[2], w[2], Q[2], sq[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      u[j] = factored<double, LU, lu>(x[j], R.uq, R.ul);
+      v[j] = factored<double, LV, lv>(x[j], R.vq, R.vl);
+    }
+    bool s0, s1;
+    w[0] = A::div_fast(u[0], v[0], s0);
+    w[1] = A::div_fast(u[1], v[1], s1);
+    if (__any_sync(kFull, s0 || s1)) { w[0] = A::div(u[0], v[0]); w[1] = A::div(u[1], v[1]); }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      double h = A::mul(R.q2, w[j]);
+      h = A::fma(h, x[j], R.q1);
+      Q[j] = A::fma(h, x[j], R.q0);
+    }
+    sq[0] = A::sqrt_fast(Q[0], s0);
+    sq[1] = A::sqrt_fast(Q[1], s1);
+    if (__any_sync(kFull, s0 || s1)) { sq[0] = A::sqrt(Q[0]); sq[1] = A::sqrt(Q[1]); }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const double s = n == 0 ? sq[j] : A::mul(powi<double, (n == 0 ? 1 : n)>(Q[j]), sq[j]);
+      const double yq = A::fma(s, t[j], x[j]);
+      y[j] = x[j] < R.z ? yq : x[j];
+    }
+  }
+  double r[2], sr[2];
+  bool s0, s1;
+  r[0] = A::rcp_fast(y[0], s0);
+  r[1] = A::rcp_fast(y[1], s1);
+  if (__any_sync(kFull, s0 || s1)) { r[0] = A::rcp(y[0]); r[1] = A::rcp(y[1]); }
+  sr[0] = A::sqrt_fast(r[0], s0);
+  sr[1] = A::sqrt_fast(r[1], s1);
+  if (__any_sync(kFull, s0 || s1)) { sr[0] = A::sqrt(r[0]); sr[1] = A::sqrt(r[1]); }
+#pragma unroll
+  for (int j = 0; j < 2; ++j)
+    F[j] = n == 0 ? A::mul(R.c, sr[j])
+                  : A::mul(A::mul(R.c, powi<double, (n == 0 ? 1 : n)>(r[j])), sr[j]);
+}
+
+// Two adjacent points per thread, evaluated in lockstep: per point the same
+// operation sequence as eval_point_stream (so the same bits); put(m, a, b)
+// receives F_m of both points at once so a SoA row takes one 16-byte store.
+// The warp-uniform shortcuts see 64 points instead of 32 (values unchanged).
+template <typename T, int n, typename Put, typename Put1>
+__device__ __forceinline__ void eval_pair_stream(T xa, T xb, bool oka, bool okb, T& ta_out,
+                                                 T& tb_out, Put&& put, Put1&& put1) {
+  using A = Ar<T>;
+  const BoysRow<T>& R = Tab<T>::row(n);
+  const T bad = A::nan();
+  T x[2] = {oka ? xa : bad, okb ? xb : bad};
+  const bool ok[2] = {oka, okb};
+  T t[2], cur[2], tx[2];
+  bool below = false, up = false;
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    t[j] = exp_neg_clamped(x[j]);
+    below = below || (ok[j] && x[j] < R.z);
+  }
+  const bool any_below = __any_sync(kFull, below);
+#if BOYS_PAIR_FASTCR
+  if constexpr (sizeof(T) == 8) seed_pair<n>(x, t, any_below, cur);
+  else
+#endif
+  {
+#pragma unroll
+    for (int j = 0; j < 2; ++j) cur[j] = seed<T, n>(x[j], t[j], any_below);
+  }
+  put(n, cur[0], cur[1]);
+#pragma unroll
+  for (int j = 0; j < 2; ++j) tx[j] = A::add(x[j], x[j]);
+#pragma unroll
+  for (int m = n - 1; m >= 0; --m) {
+#pragma unroll
+    for (int j = 0; j < 2; ++j) cur[j] = A::mul(A::fma(tx[j], cur[j], t[j]), rinv<T>(m));
+    put(m, cur[0], cur[1]);
+  }
+#pragma unroll
+  for (int j = 0; j < 2; ++j) up = up || (ok[j] && x[j] > R.x_up);
+  if (__any_sync(kFull, up)) {
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const bool upj = ok[j] && x[j] > R.x_up;
+      T rx = A::rcp(x[j]);
+      T f = up_first(x[j]);
+      if (upj) put1(j, 0, f);
+#pragma unroll
+      for (int m = 0; m < n; ++m) {
+        f = up_next(f, m, rx);
+        if (upj) put1(j, m + 1, f);
+      }
+    }
+  }
+  ta_out = oka ? t[0] : bad;
+  tb_out = okb ? t[1] : bad;
+}
+
+// ---------------------------------------------------------------------------
+// run-time-order evaluation (ragged / split)
+// ---------------------------------------------------------------------------
+// Row accessors for the run-time-order evaluator: rows staged in shared
+// memory (ragged fast path: per-lane orders) or read from __constant__
+// (split: warp-uniform order -> broadcast; rare high-order ragged chunks).
+template <typename T, int R>
+struct SmemTable {
+  BoysRow<T> row[R];
+};
+
+template <typename T, int R>
+__device__ __forceinline__ void stage_table(SmemTable<T, R>& st) {
+  static_assert(sizeof(BoysRow<T>) % sizeof(int) == 0, "row layout");
+  constexpr int words = R * sizeof(BoysRow<T>) / sizeof(int);
+  const int* src = reinterpret_cast<const int*>(&Tab<T>::row(0));
+  int* dst = reinterpret_cast<int*>(&st.row[0]);
+  for (int k = threadIdx.x; k < words; k += blockDim.x) dst[k] = src[k];
+}
+
+template <typename T>
+struct SmemRows {
+  const BoysRow<T>* p;
+  __device__ __forceinline__ const BoysRow<T>& operator()(int n) const { return p[n]; }
+};
+template <typename T>
+struct ConstRows {
+  __device__ __forceinline__ const BoysRow<T>& operator()(int n) const { return Tab<T>::row(n); }
+};
+
+template <typename T> struct MaxShape;   // compile-time bounds on factor counts
+template <> struct MaxShape<double> {
+  __host__ __device__ static constexpr int Q() {
+    int m = 0;
+    for (int n = 0; n <= BOYS_F64_MAX_ORDER; ++n)
+      for (int k : {0, 2}) m = boys_shape_f64(n, k) > m ? boys_shape_f64(n, k) : m;
+    return m;
+  }
+  __host__ __device__ static constexpr int L() {
+    int m = 0;
+    for (int n = 0; n <= BOYS_F64_MAX_ORDER; ++n)
+      for (int k : {1, 3}) m = boys_shape_f64(n, k) > m ? boys_shape_f64(n, k) : m;
+    return m;
+  }
+};
+template <> struct MaxShape<float> {
+  __host__ __device__ static constexpr int Q() {
+    int m = 0;
+    for (int n = 0; n <= BOYS_F32_MAX_ORDER; ++n)
+      for (int k : {0, 2}) m = boys_shape_f32(n, k) > m ? boys_shape_f32(n, k) : m;
+    return m;
+  }
+  __host__ __device__ static constexpr int L() {
+    int m = 0;
+    for (int n = 0; n <= BOYS_F32_MAX_ORDER; ++n)
+      for (int k : {1, 3}) m = boys_shape_f32(n, k) > m ? boys_shape_f32(n, k) : m;
+    return m;
+  }
+};
+
+// y = x + Q~^{n+1/2} e^{-x} below the cut-off, run-time order; identical
+// operation sequence to seed<T, n>'s Q~ branch.
+template <typename T, typename Rows>
+__device__ __forceinline__ T y_below_rt(T x, T t, int n, const Rows& rows) {
+  using A = Ar<T>;
+  constexpr int MQ = MaxShape<T>::Q(), ML = MaxShape<T>::L();
+  const BoysRow<T>& R = rows(n);
+  T u = factored_rt<T, MQ, ML>(x, R.uq, R.ul, R.cnt[0], R.cnt[1]);
+  T v = factored_rt<T, MQ, ML>(x, R.vq, R.vl, R.cnt[2], R.cnt[3]);
+  T w = A::div(u, v);
+  T h = A::mul(R.q2, w);
+  h = A::fma(h, x, R.q1);
+  T Q = A::fma(h, x, R.q0);
+  T sq = A::sqrt(Q);
+  T s = n == 0 ? sq : A::mul(powi_rt(Q, n), sq);
+  return A::fma(s, t, x);
+}
+
+// b^n for n < 2^bits (bits: warp-uniform bound); same products as powi<T,n>:
+// starting from 1.0 and multiplying by (bit ? b^(2^j) : 1.0) is exact for the
+// unset bits (x * 1.0 == x) and 1.0 * b^(2^j0) == b^(2^j0) for the first set
+// bit, so the rounded product sequence is identical -- with one select per
+// step instead of a select over a conditional product.
+template <typename T>
+__device__ __forceinline__ T powi_rt_bounded(T b, int n, int bits) {
+  using A = Ar<T>;
+  // j = 0: 1.0 * b == b exactly, so a select (n < 2^bits with bits >= 1)
+  T r = (n & 1) ? b : T(1), p = b;
+#pragma unroll
+  for (int j = 1; j < 6; ++j) {
+    if (j >= bits) break;
+    p = A::mul(p, p);
+    r = A::mul(r, ((n >> j) & 1) ? p : T(1));
+  }
+  return r;
+}
+
+// Tail for a run-time order n (per lane): F_n from y, then the recursion and
+// the upward ladder, handed to put(m, v, on): `on` says whether m <= n, i.e.
+// whether the value is one of this lane's outputs (callers store
+// unconditionally to a scratch slot otherwise, so the loop stays branch-free).
+// `wmax` = warp-uniform max order bounds the loops.
+template <typename T, int NB, typename Rows, typename Put>
+__device__ __forceinline__ void tail_rt(T x, T y, T t, int n, bool ok, int wmax,
+                                        const Rows& rows, Put&& put) {
+  using A = Ar<T>;
+  const T bad = A::nan();
+  const int bits = 32 - __clz(wmax | 1);
+  T r = A::rcp(y);
+  T sr = A::sqrt(r);
+  const T c = rows(n).c;
+  T cur = A::mul(A::mul(c, powi_rt_bounded(r, n, bits)), sr);   // n = 0: exact, see above
+  put(n, ok ? cur : bad, true);
+  T tx = A::add(x, x);
+#pragma unroll
+  for (int m = NB - 1; m >= 0; --m) {
+    if (m < wmax) {                                // warp-uniform
+      T nx = A::mul(A::fma(tx, cur, t), rinv<T>(m));
+      const bool on = m < n;
+      cur = on ? nx : cur;
+      put(m, ok ? cur : bad, on);
+    }
+  }
+  bool up = ok && x > rows(n).x_up;
+  if (__any_sync(kFull, up)) {
+    T rx = A::rcp(x);
+    T f = up_first(x);
+    if (up) put(0, f, true);
+#pragma unroll
+    for (int m = 0; m < NB; ++m) {
+      if (m >= wmax) break;
+      f = up_next(f, m, rx);
+      if (up && m + 1 <= n) put(m + 1, f, true);
+    }
+  }
+}
+
+// Root-factored product with a warp-uniform run-time factor count: the
+// active steps of factored_rt (same products, same order), skipping the
+// inactive ones with a uniform branch instead of selecting them away.
+template <typename T, int MQ, int ML>
+__device__ __forceinline__ T factored_uniform(T x, const T (*q)[2], const T* l, int nq, int nl) {
+  using A = Ar<T>;
+  T acc = T(1);
+  bool first = true;
+#pragma unroll
+  for (int k = 0; k < MQ; ++k) {
+    if (k >= nq) break;
+    T d = A::sub(x, q[k][0]);
+    T f = A::fma(d, d, q[k][1]);
+    acc = first ? f : A::mul(acc, f);
+    first = false;
+  }
+#pragma unroll
+  for (int k = 0; k < ML; ++k) {
+    if (k >= nl) break;
+    T f = A::sub(x, l[k]);
+    acc = first ? f : A::mul(acc, f);
+    first = false;
+  }
+  return acc;
+}
+
+// eval_point_rt for an order that is the same on every lane of the warp
+// (split kernel): uniform loop bounds instead of per-lane selects.  Invalid
+// lanes evaluate x = 0 at that order and output NaN, as in eval_point_rt.
+template <typename T, int NB, typename Rows, typename Put>
+__device__ __forceinline__ void eval_point_uniform(T x_in, bool ok, int n, const Rows& rows,
+                                                   Put&& put) {
+  using A = Ar<T>;
+  constexpr int MQ = MaxShape<T>::Q(), ML = MaxShape<T>::L();
+  T x = ok ? x_in : T(0);
+  T t = exp_neg_clamped(x);
+  const BoysRow<T>& R = rows(n);
+  bool below = ok && x < R.z;
+  T y = x;
+  if (__any_sync(kFull, below)) {
+    T u = factored_uniform<T, MQ, ML>(x, R.uq, R.ul, R.cnt[0], R.cnt[1]);
+    T v = factored_uniform<T, MQ, ML>(x, R.vq, R.vl, R.cnt[2], R.cnt[3]);
+    T w = A::div(u, v);
+    T h = A::mul(R.q2, w);
+    h = A::fma(h, x, R.q1);
+    T Q = A::fma(h, x, R.q0);
+    T sq = A::sqrt(Q);
+    T s = n == 0 ? sq : A::mul(powi_rt_bounded(Q, n, 32 - __clz(n | 1)), sq);
+    T yq = A::fma(s, t, x);
+    y = below ? yq : x;
+  }
+  tail_rt<T, NB>(x, y, t, n, ok, n, rows, [&](int m, T v, bool on) {
+    if (on) put(m, v);
+  });
+}
+
+// Complete run-time-order evaluation (split kernel; ragged fallback tiles).
+template <typename T, int NB, typename Rows, typename Put>
+__device__ __forceinline__ void eval_point_rt(T x_in, bool ok, int n, const Rows& rows,
+                                              Put&& put) {
+  using A = Ar<T>;
+  T x = ok ? x_in : T(0);
+  int ns = ok ? n : 0;
+  T t = exp_neg_clamped(x);
+  bool below = ok && x < rows(ns).z;
+  T y = x;
+  if (__any_sync(kFull, below)) {
+    T yq = y_below_rt(x, t, ns, rows);
+    y = below ? yq : x;
+  }
+  int wmax = __reduce_max_sync(kFull, (unsigned)ns);
+  tail_rt<T, NB>(x, y, t, ns, ok, wmax, rows, [&](int m, T v, bool on) {
+    if (on) put(m, v);
+  });
+}
+
+}  // namespace boys

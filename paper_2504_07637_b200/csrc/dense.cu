@@ -1,0 +1,265 @@
+// Dense kernels (one order for the whole batch): the paired SoA kernel, the
+// one-point SoA / AoS kernel, and their launch rules.  Part of libboys.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <type_traits>
+
+#include "boys_device.cuh"
+#include "boys_launch.h"
+
+namespace boys {
+
+// SoA dense kernel, two adjacent points per thread (512-point tiles): x comes
+// in as one 16-byte load and every F_m row leaves as 16-byte streaming stores
+// (512 contiguous bytes per warp instruction, half the store instructions).
+// Requires N even and 16-byte aligned x/out/expx (host checks).
+template <typename T, int n, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
+dense_soa_pair_kernel(const T* __restrict__ X, int64_t N, T* __restrict__ out,
+                      T* __restrict__ expx, int64_t* __restrict__ dom, int64_t index_base) {
+  using V2 = typename std::conditional<sizeof(T) == 8, double2, float2>::type;
+  const int tid = threadIdx.x;
+  constexpr int TILE = 2 * kThreads;
+  const int64_t ntiles = (N + TILE - 1) / TILE;
+  pdl_wait_and_release();
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t i = tile * TILE + 2 * tid;     // even; N even => i + 1 < N iff i < N
+    const bool in = i < N;
+    V2 xv;
+    if (in) xv = __ldg(reinterpret_cast<const V2*>(X + i));
+    else { xv.x = T(0); xv.y = T(0); }
+    bool oka = valid_x(xv.x), okb = valid_x(xv.y);
+    if (in && !oka) flag_domain(dom, index_base + i);
+    if (in && !okb) flag_domain(dom, index_base + i + 1);
+    oka = oka || !in;
+    okb = okb || !in;
+    T* o = out + i;
+    T ta, tb;
+    eval_pair_stream<T, n>(
+        xv.x, xv.y, oka, okb, ta, tb,
+        [&](int m, T a, T b) {
+          V2 v;
+          v.x = a;
+          v.y = b;
+          if (in) __stcs(reinterpret_cast<V2*>(o + (int64_t)m * N), v);
+        },
+        [&](int j, int m, T v) {
+          if (in) __stcs(o + (int64_t)m * N + j, v);
+        });
+    if (expx && in) {
+      V2 tv;
+      tv.x = ta;
+      tv.y = tb;
+      __stcs(reinterpret_cast<V2*>(expx + i), tv);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// dense kernel
+// ---------------------------------------------------------------------------
+template <typename T, int n, bool AOS, int NBUF, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
+dense_kernel(const T* __restrict__ X, int64_t N, T* __restrict__ out, T* __restrict__ expx,
+             int64_t* __restrict__ dom, int64_t index_base, bool bulk_ok, bool soa_bulk) {
+  constexpr int W = n + 1;
+  constexpr int TILE_ELEMS = kThreads * W;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  T* sbase = reinterpret_cast<T*>(smem_raw);
+  const int tid = threadIdx.x;
+  const int64_t ntiles = (N + kThreads - 1) / kThreads;
+  pdl_wait_and_release();
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const int64_t i0 = tile * kThreads;
+    const int64_t i = i0 + tid;
+    const bool in = i < N;
+    // (loading the next tile's x one iteration ahead measured slower:
+    // SoA 77% vs 84%, AoS 86% vs 94% of HBM, tools/ab/ab25.sh)
+    const T x = in ? ldg_nc(X + i) : T(0);
+    bool ok = valid_x(x);
+    if (in && !ok) flag_domain(dom, index_base + i);
+    ok = ok || !in;   // tail lanes evaluate x = 0 quietly
+    if constexpr (!AOS) {
+      if (soa_bulk) {
+        // [n+1][256] tile in shared memory, one bulk copy per order row
+        T* buf = sbase + (it % NBUF) * TILE_ELEMS;
+        if (tid == 0) bulk_wait_read<NBUF - 1>();
+        __syncthreads();
+        T t = eval_point_stream<T, n>(x, ok, [&](int m, T v) { buf[m * kThreads + tid] = v; });
+        if (expx && in) __stcs(expx + i, t);
+        const int64_t cnt = (N - i0) < kThreads ? (N - i0) : kThreads;
+        if (cnt == kThreads) {
+          fence_proxy_async_smem();
+          __syncthreads();
+          if (tid < W) bulk_store(out + (int64_t)tid * N + i0, buf + tid * kThreads,
+                                  kThreads * sizeof(T));
+        } else {
+          __syncthreads();
+          for (int k = tid; k < W * kThreads; k += kThreads) {
+            const int m = k / kThreads, j = k % kThreads;
+            if (j < cnt) __stcs(out + (int64_t)m * N + i0 + j, buf[k]);
+          }
+        }
+      } else {
+        T* o = out + i;
+        T t = eval_point_stream<T, n>(x, ok, [&](int m, T v) {
+          if (in) __stcs(o + (int64_t)m * N, v);
+        });
+        if (expx && in) __stcs(expx + i, t);
+      }
+    } else {
+      T* buf = sbase + (it % NBUF) * TILE_ELEMS;
+      // the slot went to the bulk engine NBUF tiles ago: wait until it was read
+      if (tid == 0) bulk_wait_read<NBUF - 1>();
+      __syncthreads();
+      T* row = buf + tid * W;
+      T t = eval_point_stream<T, n>(x, ok, [&](int m, T v) { row[m] = v; });
+      if (expx && in) __stcs(expx + i, t);
+      const int64_t cnt = (N - i0) < kThreads ? (N - i0) : kThreads;
+      if (bulk_ok && cnt == kThreads) {
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (tid == 0) bulk_store(out + i0 * W, buf, TILE_ELEMS * sizeof(T));
+      } else {
+        __syncthreads();
+        T* dst = out + i0 * W;
+        for (int k = tid; k < cnt * W; k += kThreads) __stcs(dst + k, buf[k]);
+      }
+    }
+  }
+  if (AOS || soa_bulk) {
+    if (tid < (AOS ? 1 : W)) bulk_wait_all();
+  }
+}
+
+template <typename T, int n, bool AOS, int NBUF, int MINB>
+static boys_status launch_dense_k(const T* x, int64_t N, T* out, T* expx, int64_t* dom,
+                                  int64_t base, cudaStream_t s) {
+  auto k = dense_kernel<T, n, AOS, NBUF, MINB>;
+  // SoA bulk rows need every row start 16-byte aligned: N * sizeof(T) % 16 == 0
+  const bool soa_bulk = !AOS && soa_tma() && (N * (int64_t)sizeof(T)) % 16 == 0 &&
+                        (reinterpret_cast<uintptr_t>(out) % 16) == 0;
+  size_t smem = (AOS || soa_bulk) ? (size_t)NBUF * kThreads * (n + 1) * sizeof(T) : 0;
+  // the dynamic-smem opt-in is per function *per device*: remember each device
+  static std::atomic<uint64_t> attr_mask{0};
+  {
+    const int smem_max = (int)((size_t)NBUF * kThreads * (n + 1) * sizeof(T));
+    boys_status st = opt_in_smem(k, smem_max, attr_mask);
+    if (st != BOYS_OK) return st;
+  }
+  int64_t ntiles = (N + kThreads - 1) / kThreads;
+  bool bulk_ok = (reinterpret_cast<uintptr_t>(out) % 16) == 0;
+  // Grid: persistent (SMs x resident blocks) or one block per tile, chosen
+  // by same-box measurement (tools/ab/ab29.sh, ab30.sh; graph-replayed
+  // streams at 2^20..2^24 points): one block per tile wins for f64 SoA at
+  // n <= 5 and n >= 11 (n=0: 143 vs 154 us, n=16: 398 vs 471 us at 2^24),
+  // persistent for f64 SoA n = 6..10 (n=8: 265 vs 282 us), for f32 SoA and for
+  // AoS (whose double-buffered bulk stores need the loop).  BOYS_GRID_TILES=1/2
+  // forces one or the other.
+  int grid = blocks_for(k, smem, ntiles);
+  const int gt = grid_tiles();
+  const bool per_tile = gt == 1 || (gt == 0 && !AOS && !soa_bulk && sizeof(T) == 8 &&
+                                    (n <= 5 || n >= 11));
+  if (per_tile && ntiles <= (int64_t)1 << 30) grid = (int)ntiles;
+  if (pdl()) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k, x, N, out, expx, dom, base, bulk_ok, soa_bulk);
+    if (e != cudaSuccess) return cuda_status(e);
+  } else {
+    k<<<grid, kThreads, smem, s>>>(x, N, out, expx, dom, base, bulk_ok, soa_bulk);
+  }
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cuda_status(cudaGetLastError());
+}
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+template <typename T, int n>
+static boys_status launch_soa_pair(const T* x, int64_t N, T* out, T* expx, int64_t* dom,
+                                   int64_t base, cudaStream_t s) {
+  constexpr int MINB = n <= 1 ? BOYS_PAIR_MINB_SMALL : BOYS_SOA_MINB;   // two chains: 8 blocks would spill at n = 0
+  auto k = dense_soa_pair_kernel<T, n, MINB>;
+  const int64_t ntiles = (N + 2 * kThreads - 1) / (2 * kThreads);
+  int grid = blocks_for(k, 0, ntiles);
+  const int gt = grid_tiles();
+  if ((gt == 1 || (gt == 0 && soa_pair_per_tile(sizeof(T) == 8, n))) && ntiles <= ((int64_t)1 << 30))
+    grid = (int)ntiles;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl() ? 1 : 0;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k, x, N, out, expx, dom, base);
+  if (e != cudaSuccess) return cuda_status(e);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cuda_status(cudaGetLastError());
+}
+
+template <typename T, int n, bool AOS>
+static boys_status launch_dense_t(const T* x, int64_t N, T* out, T* expx, int64_t* dom,
+                                  int64_t base, cudaStream_t s) {
+  if constexpr (!AOS) {
+    constexpr bool fits2 = 2 * kThreads * (n + 1) * sizeof(T) <= 80 * 1024;
+    if (soa_tma()) return launch_dense_k<T, n, false, (fits2 ? 2 : 1), 4>(x, N, out, expx, dom, base, s);
+    if constexpr (n <= 1) {          // small orders: register budget for 6 or 8 blocks/SM
+      if (soa_small_minb() == 6) return launch_dense_k<T, n, false, 1, 6>(x, N, out, expx, dom, base, s);
+    }
+    if (soa_pair() && N % 2 == 0 && aligned16(x) && aligned16(out) && (!expx || aligned16(expx)))
+      return launch_soa_pair<T, n>(x, N, out, expx, dom, base, s);
+    return launch_dense_k<T, n, false, 1, (n <= 1 ? 8 : BOYS_SOA_MINB)>(x, N, out, expx, dom, base, s);
+  } else {
+    // double-buffer the AoS tile while two tiles fit in ~80 KB (n <= 18 in f64)
+    constexpr bool fits2 = 2 * kThreads * (n + 1) * sizeof(T) <= 80 * 1024;
+    if (fits2 && aos_nbuf() == 2)
+      return launch_dense_k<T, n, true, (fits2 ? 2 : 1), 4>(x, N, out, expx, dom, base, s);
+    if (aos_minb() == 6) return launch_dense_k<T, n, true, 1, 6>(x, N, out, expx, dom, base, s);
+    return launch_dense_k<T, n, true, 1, 4>(x, N, out, expx, dom, base, s);
+  }
+}
+
+template <typename T, int n>
+static boys_status dispatch_dense_layout(const void* x, int64_t N, void* out, boys_layout lay,
+                                         void* expx, int64_t* dom, int64_t base, cudaStream_t s) {
+  // n = 0: [N][1] and [1][N] are the same bytes; the SoA kernel (no staging)
+  // measured faster (f64 2^24: 143 vs 167 us)
+  if (lay == BOYS_AOS && n > 0)
+    return launch_dense_t<T, n, true>((const T*)x, N, (T*)out, (T*)expx, dom, base, s);
+  return launch_dense_t<T, n, false>((const T*)x, N, (T*)out, (T*)expx, dom, base, s);
+}
+
+template <typename T, int n = 0>
+static boys_status dispatch_dense(int nmax, const void* x, int64_t N, void* out, boys_layout lay,
+                                  void* expx, int64_t* dom, int64_t base, cudaStream_t s) {
+  if constexpr (n > Tab<T>::MAX_ORDER) {
+    return BOYS_E_ORDER;
+  } else {
+    if (nmax == n) return dispatch_dense_layout<T, n>(x, N, out, lay, expx, dom, base, s);
+    return dispatch_dense<T, n + 1>(nmax, x, N, out, lay, expx, dom, base, s);
+  }
+}
+
+boys_status eval_dense_base(boys_dtype dtype, int n_max, const void* x, int64_t N,
+                            void* out, boys_layout lay, void* expx, int64_t* dom,
+                            int64_t base, cudaStream_t s) {
+  if (dtype == BOYS_F64) return dispatch_dense<double>(n_max, x, N, out, lay, expx, dom, base, s);
+  return dispatch_dense<float>(n_max, x, N, out, lay, expx, dom, base, s);
+}
+
+}  // namespace boys

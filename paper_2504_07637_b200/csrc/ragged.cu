@@ -1,0 +1,512 @@
+// Ragged batches (per-element order) and their offsets scan.  Part of libboys.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <type_traits>
+
+#include "boys_device.cuh"
+#include "boys_launch.h"
+
+namespace boys {
+
+// ---------------------------------------------------------------------------
+// ragged kernel: element i, order n_i, values at out[offsets[i] + m]
+//
+// Warp-autonomous (no block barriers): each warp walks chunks of 32*EPL elements.
+//   * every lane: e^{-x}; elements past their cut-off (x >= z_{n_i}, ~95% of
+//     ERI-like batches) run the cheap run-time-order tail at once into the
+//     warp's staging slot; the chunk's contiguous output range then leaves
+//     with coalesced streaming stores (skipping deferred elements).
+//   * elements below their cut-off are deferred to a warp-private queue and
+//     evaluated 32 at a time with every lane busy (Q~ is the expensive part),
+//     each lane writing its element's n+1 values directly.
+// Values are bit-identical to boys_eval_dense at each element's order.
+// ---------------------------------------------------------------------------
+// EPL elements per lane (chunks of 32*EPL elements): the warp-uniform work of
+// a chunk (ballots, jump-table dispatch, bulk store, constant loads) is shared
+// by EPL elements per lane, whose independent chains also interleave (ILP).
+// Staging holds CAP values; a chunk whose output range exceeds it takes the
+// per-element direct-write path (never for ERI-like order mixes).
+// CPE: staging values per element (NB + 1 = no overflow possible).
+// MINB: __launch_bounds__ min blocks per SM (0 = unconstrained).
+template <typename T, int NB, int EPL, int CPE>
+struct RaggedWarp {
+  static constexpr int CAP = 32 * EPL * (CPE < NB + 1 ? CPE : NB + 1);
+  static constexpr int QCAP = 32 * EPL + 32;      // < 32 left after a drain + one chunk
+  alignas(16) T stage[CAP + 16 / sizeof(T)];
+  T qx[QCAP], qt[QCAP];
+  int64_t qoff[QCAP];
+  unsigned char qn[QCAP];
+  T scratch[32];
+};
+
+template <typename T> struct alignas(4 * sizeof(T)) ZcRow { T z, c, x_up, pad; };  // per order
+
+template <typename T, int NB, int EPL, int CPE, int WT = kThreads>
+struct RaggedSmem {
+  SmemTable<T, NB + 1> st;           // rows 0..NB (the fast path's orders)
+  ZcRow<T> zc[NB + 1];               // per-order scalars, one 16/32-byte line each
+  RaggedWarp<T, NB, EPL, CPE> w[WT / 32];
+};
+
+// Elements above x_up(n) (upward-ladder branch) join the queue in fp32, where
+// x_up is low (2^7..2^60: ~2% of ERI-like elements; 1.00 vs 1.10 ms); in fp64
+// x_up >= 2^60 and the chunk path keeps a (never taken) ladder, which
+// measured 1.8% faster than queueing.
+template <typename T> constexpr bool kDeferUp = sizeof(T) == 4;
+
+// Evaluate up to 32 queued elements (one per lane), writing straight to
+// global memory.
+template <typename T, int NB, typename WarpT>
+__device__ __forceinline__ void ragged_drain(WarpT& W, const SmemRows<T>& st,
+                                             int& qn, int lane, T* __restrict__ out) {
+  // queued elements' slots were written (with stale staging data) by earlier
+  // bulk stores of their chunks: those must be complete before we overwrite
+  if (lane == 0) bulk_wait_all();
+  __syncwarp();
+  const int take = qn < 32 ? qn : 32;
+  const bool has = lane < take;
+  const int slot = qn - take + lane;            // LIFO: drain the newest `take` entries
+  const T x = has ? W.qx[slot] : T(0);
+  const T t = has ? W.qt[slot] : T(0);
+  const int n = has ? (int)W.qn[slot] : 0;
+  const int64_t off = has ? W.qoff[slot] : 0;
+  __syncwarp();
+  // queued: below the cut-off (Q~ branch) or above x_up (asymptotic branch,
+  // values from the upward ladder inside tail_rt)
+  T y = x;
+  if (kDeferUp<T>) {
+    const bool below = has && x < st(n).z;
+    if (__any_sync(kFull, below)) {
+      const T yq = y_below_rt(x, t, n, st);
+      y = below ? yq : x;
+    }
+  } else {
+    y = has ? y_below_rt(x, t, n, st) : x;
+  }
+  const int wmax = __reduce_max_sync(kFull, (unsigned)n);
+  T* dst = out + off;
+  T* sink = W.scratch + lane;
+  tail_rt<T, NB>(x, y, t, n, has, wmax, st,
+                 [&](int m, T v, bool on) { *((has && on) ? dst + m : sink) = v; });
+  qn -= take;
+}
+
+// Staging sentinel for deferred elements' slots: a NaN payload the arithmetic
+// never produces (IEEE ops return the canonical quiet NaN).
+template <typename T> struct Sentinel;
+template <> struct Sentinel<double> {
+  static __device__ __forceinline__ double value() { return __longlong_as_double(0x7ff4c0de5e47e1e1LL); }
+  static __device__ __forceinline__ bool is(double v) { return __double_as_longlong(v) == 0x7ff4c0de5e47e1e1LL; }
+};
+template <> struct Sentinel<float> {
+  static __device__ __forceinline__ float value() { return __int_as_float(0x7fa0c0de); }
+  static __device__ __forceinline__ bool is(float v) { return __float_as_int(v) == 0x7fa0c0de; }
+};
+
+template <typename T, int NB, int EPL, int CPE, int MINB, int WT = kThreads>
+__global__ void __launch_bounds__(WT, MINB)
+ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
+              const int64_t* __restrict__ OFF, int64_t N, T* __restrict__ out,
+              int64_t* __restrict__ dom) {
+  using A = Ar<T>;
+  using WarpT = RaggedWarp<T, NB, EPL, CPE>;
+  constexpr int CH = 32 * EPL;                   // elements per chunk
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  using SmemT = RaggedSmem<T, NB, EPL, CPE, WT>;
+  SmemT& S = *reinterpret_cast<SmemT*>(smem_raw);
+  stage_table(S.st);
+  for (int k = threadIdx.x; k <= NB; k += blockDim.x)
+    S.zc[k] = ZcRow<T>{Tab<T>::row(k).z, Tab<T>::row(k).c, Tab<T>::row(k).x_up, T(0)};
+  __syncthreads();
+  const SmemRows<T> rows{S.st.row};
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  WarpT& W = S.w[wid];
+  const int64_t nchunks = (N + CH - 1) / CH;
+  const int64_t wstride = (int64_t)gridDim.x * (WT / 32);
+  int qn = 0;                                    // warp-uniform queue length
+  int64_t c = (int64_t)blockIdx.x * (WT / 32) + wid;
+  // software pipeline: inputs of chunk c are loaded one iteration ahead
+  T px[EPL];
+  int pn[EPL];
+  int64_t poff[EPL], pbase = 0, plast_off = 0;
+  int prem = 0;                                  // elements of the prefetched chunk
+  auto load = [&](int64_t cc) {
+    const int64_t j0 = cc * CH;
+    if (j0 + CH <= N) {                          // full chunk (warp-uniform): no predicates
+      prem = CH;
+      const T* xp = X + j0 + lane;
+      const uint8_t* np = NM + j0 + lane;
+      const int64_t* op = OFF + j0 + lane;
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) {
+        px[e] = ldg_nc(xp + 32 * e);
+        pn[e] = (int)np[32 * e];
+        poff[e] = __ldg(op + 32 * e);
+      }
+    } else {
+      // elements of chunk cc that exist (warp-uniform, 0 past the end)
+      const int rem = cc < nchunks ? (int)(N - j0) : 0;
+      prem = rem;
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) {
+        const int64_t j = j0 + 32 * e + lane;
+        const bool jin = 32 * e + lane < rem;
+        px[e] = jin ? ldg_nc(X + j) : T(0);
+        pn[e] = jin ? (int)NM[j] : 0;
+        poff[e] = jin ? __ldg(OFF + j) : 0;
+      }
+    }
+    if (cc < nchunks) {
+      pbase = __ldg(OFF + j0);
+      plast_off = __ldg(OFF + ((j0 + CH < N) ? j0 + CH : N));
+    }
+  };
+  load(c);
+  for (; c < nchunks; c += wstride) {
+    const int64_t i0 = c * CH;
+    T x[EPL];
+    int n[EPL];
+    int64_t goff[EPL];
+    bool in[EPL];
+    const int rem = prem;
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) {
+      x[e] = px[e];
+      n[e] = pn[e];
+      goff[e] = poff[e];
+      in[e] = 32 * e + lane < rem;
+    }
+    const int64_t base = pbase, cnt = plast_off - pbase;
+    load(c + wstride);
+    constexpr int MAXN = Tab<T>::MAX_ORDER;
+    bool xok[EPL], slow = cnt > WarpT::CAP;
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) {
+      xok[e] = valid_x(x[e]);
+      if (in[e] && !(xok[e] && n[e] <= MAXN)) flag_domain(dom, i0 + 32 * e + lane);
+      slow = slow || (in[e] && n[e] > NB);
+    }
+    if (__any_sync(kFull, slow)) {
+      // an order above the fast path's bound (or an output range above the
+      // staging capacity): every lane evaluates its own elements from the
+      // __constant__ rows and writes them directly (NaN above the table)
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) {
+        if (in[e] && n[e] > MAXN) {
+          for (int m = 0; m <= n[e]; ++m) out[goff[e] + m] = A::nan();
+        }
+        const bool okl = in[e] && xok[e] && n[e] <= MAXN;
+        T* dst = out + goff[e];
+        const bool wd = in[e] && n[e] <= MAXN;
+        eval_point_rt<T, MAXN>(x[e], okl, okl ? n[e] : 0, ConstRows<T>{}, [&](int m, T v) {
+          if (wd) dst[m] = v;
+        });
+      }
+      continue;
+    }
+    // staging position matches the global 16-byte phase of the chunk range
+    constexpr int Q = 16 / sizeof(T);
+    const int shift = (int)(base & (Q - 1));
+    // the previous chunk's bulk store must have finished reading the slot
+    if (lane == 0) bulk_wait_read<0>();
+    __syncwarp();
+    T xs[EPL], t[EPL], cur[EPL], tx[EPL];
+    ZcRow<T> zc[EPL];
+    T* dst[EPL];
+    bool wr[EPL];
+    int wmax_l = 0;
+    // (evaluating e^{-x} only for the elements with x <= XEXP, compacted one
+    // per lane, measured no faster: tools/ab/ab24.sh)
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) {
+      const bool ok = in[e] && xok[e];
+      xs[e] = ok ? x[e] : A::nan();                // NaN propagates through the tail
+      const T xe = ok ? x[e] : T(0);
+      t[e] = exp_neg_clamped(xe);
+      zc[e] = S.zc[n[e]];
+      // deferred to the warp queue: below the cut-off (Q~ needed) and, in
+      // fp32, above x_up (upward ladder)
+      const bool defer = ok && (xe < zc[e].z || (kDeferUp<T> && xe > zc[e].x_up));
+      const unsigned dmask = __ballot_sync(kFull, defer);
+      dst[e] = W.stage + (int)(goff[e] - base) + shift;
+      if (dmask) {                                 // enqueue (qn stays warp-uniform)
+        if (defer) {
+          const int slot = qn + __popc(dmask & ((1u << lane) - 1u));
+          W.qx[slot] = xe;
+          W.qt[slot] = t[e];
+          W.qn[slot] = (unsigned char)n[e];
+          W.qoff[slot] = goff[e];
+        }
+        qn += __popc(dmask);
+      }
+      wr[e] = in[e] && !defer;
+      wmax_l = max(wmax_l, wr[e] ? n[e] : 0);
+    }
+    // immediate elements (past the cut-off): y = x.  Same operation sequence
+    // as seed<T, n> + the recursion (+ the upward ladder in fp64).
+    {
+      const int wmax = __reduce_max_sync(kFull, (unsigned)wmax_l);
+      const int bits = 32 - __clz(wmax | 1);
+      T r[EPL], sr[EPL];
+#if BOYS_FAST_CR
+      // correctly rounded 1/x and sqrt through the branch-free fast paths for
+      // all EPL elements at once (interleaved chains); the rare slow-path
+      // lanes (x near 0 / the exponent limits, NaN) recompute with the intrinsics
+      {
+        bool slow = false;
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) {
+          bool s1;
+          r[e] = A::rcp_fast(xs[e], s1);
+          slow = slow || s1;
+        }
+        if (__any_sync(kFull, slow)) {
+#pragma unroll
+          for (int e = 0; e < EPL; ++e) r[e] = A::rcp(xs[e]);
+        }
+        slow = false;
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) {
+          bool s2;
+          sr[e] = A::sqrt_fast(r[e], s2);
+          slow = slow || s2;
+        }
+        if (__any_sync(kFull, slow)) {
+#pragma unroll
+          for (int e = 0; e < EPL; ++e) sr[e] = A::sqrt(r[e]);
+        }
+      }
+#else
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) {
+        r[e] = A::rcp(xs[e]);
+        sr[e] = A::sqrt(r[e]);
+      }
+#endif
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) {
+        const T cn = zc[e].c;
+        // n = 0: powi gives exactly 1.0 and (c * 1.0) * sr == c * sr, so no select
+        cur[e] = A::mul(A::mul(cn, powi_rt_bounded(r[e], n[e], bits)), sr[e]);
+        if (wr[e]) dst[e][n[e]] = cur[e];
+        tx[e] = A::add(xs[e], xs[e]);
+      }
+      // recursion steps m = wmax-1 .. 0: enter the unrolled chain once through
+      // a jump table (wmax is warp-uniform) instead of testing every step
+      // one predicate per element and step: elements that are not written
+      // here (deferred, padding) take no steps (their cur is never used)
+      int neff[EPL];
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) neff[e] = wr[e] ? n[e] : 0;
+#define BOYS_STEP(M)                                                       \
+  if ((M) < NB) {                                                           \
+    _Pragma("unroll") for (int e = 0; e < EPL; ++e) {                       \
+      const T nx = A::mul(A::fma(tx[e], cur[e], t[e]), rinv<T>((M) < NB ? (M) : 0)); \
+      const bool on = (M) < neff[e];                                        \
+      pmov(on, cur[e], nx);                                                 \
+      psts(on, dst[e] + (M), cur[e]);                                       \
+    }                                                                       \
+  }
+      switch (wmax) {
+        case 16: BOYS_STEP(15) [[fallthrough]];
+        case 15: BOYS_STEP(14) [[fallthrough]];
+        case 14: BOYS_STEP(13) [[fallthrough]];
+        case 13: BOYS_STEP(12) [[fallthrough]];
+        case 12: BOYS_STEP(11) [[fallthrough]];
+        case 11: BOYS_STEP(10) [[fallthrough]];
+        case 10: BOYS_STEP(9) [[fallthrough]];
+        case 9: BOYS_STEP(8) [[fallthrough]];
+        case 8: BOYS_STEP(7) [[fallthrough]];
+        case 7: BOYS_STEP(6) [[fallthrough]];
+        case 6: BOYS_STEP(5) [[fallthrough]];
+        case 5: BOYS_STEP(4) [[fallthrough]];
+        case 4: BOYS_STEP(3) [[fallthrough]];
+        case 3: BOYS_STEP(2) [[fallthrough]];
+        case 2: BOYS_STEP(1) [[fallthrough]];
+        case 1: BOYS_STEP(0) [[fallthrough]];
+        default: break;
+      }
+#undef BOYS_STEP
+      static_assert(NB <= 16, "extend the recursion jump table");
+      if (!kDeferUp<T>) {
+        bool up[EPL], anyup = false;
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) {
+          up[e] = wr[e] && xs[e] > zc[e].x_up;   // NaN (invalid) compares false
+          anyup = anyup || up[e];
+        }
+        if (__any_sync(kFull, anyup)) {
+#pragma unroll
+          for (int e = 0; e < EPL; ++e) {
+            const T rx = A::rcp(xs[e]);
+            T f = up_first(xs[e]);
+            if (up[e]) dst[e][0] = f;
+#pragma unroll
+            for (int m = 0; m < NB; ++m) {
+              if (m >= wmax) break;
+              f = up_next(f, m, rx);
+              if (up[e] && m + 1 <= n[e]) dst[e][m + 1] = f;
+            }
+          }
+        }
+      }
+    }
+    __syncwarp();
+    // the chunk's output range [base, base + cnt): scalar head/tail to reach
+    // 16-byte alignment, one bulk async copy (TMA engine) for the body.
+    // Deferred elements' slots go out stale and are rewritten by the drain.
+    {
+      const int ncnt = (int)cnt;
+      const int head = ((Q - shift) & (Q - 1)) < ncnt ? ((Q - shift) & (Q - 1)) : ncnt;
+      const int body = ((ncnt - head) / Q) * Q;
+      const int tail0 = head + body;
+      if (lane < head) __stcs(out + base + lane, W.stage[shift + lane]);
+      if (lane < ncnt - tail0) __stcs(out + base + tail0 + lane, W.stage[shift + tail0 + lane]);
+      if (body > 0) {
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) bulk_store(out + base + head, W.stage + shift + head, body * sizeof(T));
+      }
+    }
+    while (qn >= 32) ragged_drain<T, NB>(W, rows, qn, lane, out);
+  }
+  while (qn > 0) ragged_drain<T, NB>(W, rows, qn, lane, out);
+  if (lane == 0) bulk_wait_all();
+}
+
+// (A block-window ragged variant -- 1024-element windows counting-sorted into
+// order buckets, one compile-time-order tail per warp task -- measured slower
+// than the warp chunks for both dtypes (f64 2.59 vs 1.92 ms, f32 1.19 vs
+// 1.00 ms) and was removed; it is in the history up to commit 50d605b.)
+
+// ---------------------------------------------------------------------------
+// ragged offsets: exclusive prefix sum of (n_i + 1), single-pass per block +
+// a tiny second pass over block totals (decoupled; two launches)
+// ---------------------------------------------------------------------------
+__global__ void offsets_block_kernel(const uint8_t* __restrict__ NM, int64_t N,
+                                     int64_t* __restrict__ OFF, int64_t* __restrict__ blk) {
+  __shared__ int64_t s[kThreads];
+  const int64_t per = 8;
+  const int64_t b0 = (int64_t)blockIdx.x * kThreads * per;
+  int64_t loc[8];
+  int64_t acc = 0;
+  for (int k = 0; k < per; ++k) {
+    int64_t i = b0 + threadIdx.x * per + k;
+    loc[k] = acc;
+    acc += (i < N) ? (int64_t)NM[i] + 1 : 0;
+  }
+  s[threadIdx.x] = acc;
+  __syncthreads();
+  for (int d = 1; d < kThreads; d <<= 1) {
+    int64_t v = threadIdx.x >= d ? s[threadIdx.x - d] : 0;
+    __syncthreads();
+    s[threadIdx.x] += v;
+    __syncthreads();
+  }
+  int64_t excl = s[threadIdx.x] - acc;
+  for (int k = 0; k < per; ++k) {
+    int64_t i = b0 + threadIdx.x * per + k;
+    if (i < N) OFF[i] = excl + loc[k];
+  }
+  if (threadIdx.x == kThreads - 1) blk[blockIdx.x] = s[threadIdx.x];
+}
+
+__global__ void offsets_fix_kernel(int64_t N, int64_t nblk, int64_t* __restrict__ OFF,
+                                   const int64_t* __restrict__ blk) {
+  // every block redundantly scans the block totals it needs (nblk is small)
+  __shared__ int64_t add;
+  const int64_t per = 8;
+  const int64_t b = blockIdx.x;
+  if (threadIdx.x == 0) {
+    int64_t a = 0;
+    for (int64_t k = 0; k < b; ++k) a += blk[k];
+    add = a;
+  }
+  __syncthreads();
+  const int64_t b0 = b * kThreads * per;
+  for (int k = 0; k < per; ++k) {
+    int64_t i = b0 + threadIdx.x * per + k;
+    if (i < N) OFF[i] += add;
+  }
+  if (b == nblk - 1 && threadIdx.x == 0) {
+    int64_t a = 0;
+    for (int64_t k = 0; k < nblk; ++k) a += blk[k];
+    OFF[N] = a;
+  }
+}
+
+inline int ragged_epl() {   // BOYS_RAGGED_EPL=1: one element per lane (A/B)
+  static int v = env_int("BOYS_RAGGED_EPL", 0);
+  return v;
+}
+
+template <typename T, int NB, int EPL, int CPE, int MINB, int WT = kThreads>
+static boys_status launch_chunks(const void* x, const uint8_t* nm, const int64_t* off, int64_t N,
+                                 void* out, int64_t* dom, cudaStream_t s) {
+  auto k = ragged_kernel<T, NB, EPL, CPE, MINB, WT>;
+  const size_t smem = sizeof(RaggedSmem<T, NB, EPL, CPE, WT>);
+  static std::atomic<uint64_t> attr_mask{0};
+  boys_status st = opt_in_smem(k, (int)smem, attr_mask);
+  if (st != BOYS_OK) return st;
+  const int64_t nch = (N + 32 * EPL - 1) / (32 * EPL);
+  const int64_t nblk = (nch + WT / 32 - 1) / (WT / 32);
+  int64_t grid = blocks_for(k, smem, nblk, WT);
+  grid *= ragged_grid_mult(sizeof(T) == 8);
+  if (grid > nblk) grid = nblk;
+  k<<<(int)grid, WT, smem, s>>>((const T*)x, nm, off, N, (T*)out, dom);
+  return BOYS_OK;
+}
+
+template <typename T>
+static boys_status launch_ragged(const void* x, const uint8_t* nm, const int64_t* off, int64_t N,
+                                 void* out, int64_t* dom, cudaStream_t s) {
+  // fast-path order bound; higher orders, up to the table maximum, take the
+  // in-kernel per-element fallback path
+  constexpr int NB = Tab<T>::MAX_ORDER < kRaggedFastOrders ? Tab<T>::MAX_ORDER : kRaggedFastOrders;
+  {
+    // (order-sorted warp super-chunks were measured slower: 2.90 / 3.79 ms vs 2.42)
+    // elements per lane: measured best 3 (f64: 1.95 ms vs 2.27 / 1.97 / 2.05
+    // for 1 / 2 / 4) and 4 (f32: 1.14 ms vs 1.26 / 1.16 / 1.36 for 2 / 3 / 6)
+    constexpr int EPL = sizeof(T) == 8 ? 3 : 4;
+    // (8 instead of 12 staged values per element, or a 3-blocks/SM register
+    // bound, measured no better: 1.96 / 2.08 ms f64)
+    // (f64, 2 elements per lane with 10 staged values each, 24 warps/SM:
+    // 1.88 ms -- within 1%, but overflows to the slow path from order 10)
+    // (128-thread blocks, also with a 96-register bound and 8 staged values per
+    // element for 20 resident warps, measured slower: f64 1.84-2.36 vs 1.78 ms,
+    // f32 0.94-1.00 vs 0.94 ms, tools/ab/ab39.sh)
+    boys_status st = ragged_epl() == 1
+                         ? launch_chunks<T, NB, 1, NB + 1, 0>(x, nm, off, N, out, dom, s)
+                         : launch_chunks<T, NB, EPL, 12, 0>(x, nm, off, N, out, dom, s);
+    if (st != BOYS_OK) return st;
+  }
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cuda_status(cudaGetLastError());
+}
+
+boys_status eval_ragged_base(boys_dtype dtype, const void* x, const uint8_t* nm,
+                             const int64_t* off, int64_t N, void* out, int64_t* dom,
+                             cudaStream_t s) {
+  if (dtype == BOYS_F64) return launch_ragged<double>(x, nm, off, N, out, dom, s);
+  return launch_ragged<float>(x, nm, off, N, out, dom, s);
+}
+
+boys_status ragged_offsets_base(const uint8_t* nmax_dev, int64_t N, int64_t* offsets_dev,
+                                cudaStream_t s) {
+  if (N == 0) return cuda_status(cudaMemsetAsync(offsets_dev, 0, sizeof(int64_t), s));
+  const int64_t per_blk = (int64_t)kThreads * 8;
+  const int64_t nblk = (N + per_blk - 1) / per_blk;
+  int64_t* blk = nullptr;
+  cudaError_t e = cudaMallocAsync(&blk, nblk * sizeof(int64_t), s);
+  if (e != cudaSuccess) return cuda_status(e);
+  offsets_block_kernel<<<(unsigned)nblk, kThreads, 0, s>>>(nmax_dev, N, offsets_dev, blk);
+  offsets_fix_kernel<<<(unsigned)nblk, kThreads, 0, s>>>(N, nblk, offsets_dev, blk);
+  g_launches.fetch_add(2, std::memory_order_relaxed);
+  e = cudaGetLastError();
+  cudaFreeAsync(blk, s);
+  return cuda_status(e);
+}
+
+}  // namespace boys

@@ -1,5 +1,5 @@
 """Parity of every kernel variant reachable through an environment knob
-(the A/B switches in boys_kernels.cu are read once per process, so
+(the A/B switches in csrc/boys_launch.h are read once per process, so
 tests/test_gpu_knobs.py runs this script once per setting).
 
 Checks dense SoA/AoS (even/odd N, several orders, f64/f32), ragged (f64/f32,

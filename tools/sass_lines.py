@@ -39,7 +39,7 @@ for k, r in enumerate(data[: len(insts)]):
 ti = sum(v[0] for v in agg.values()) or 1
 ts = sum(v[1] for v in agg.values()) or 1
 src = {}
-for fn in ("boys_kernels.cu", "boys_eval.cuh"):
+for fn in ("dense.cu", "ragged.cu", "split.cu", "abi.cu", "boys_device.cuh", "boys_eval.cuh"):
     src[fn] = open(f"paper_2504_07637_b200/csrc/{fn}").read().split("\n")
 print(f"{len(insts)} SASS, {ti} warp-instr executed, {ts} stall samples")
 for (f, ln), v in sorted(agg.items(), key=lambda kv: -(kv[1][0] / ti + kv[1][1] / ts))[:int(sys.argv[5]) if len(sys.argv) > 5 else 30]:
