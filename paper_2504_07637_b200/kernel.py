@@ -302,9 +302,19 @@ def boys_ragged(x: torch.Tensor, n_max: torch.Tensor, offsets: torch.Tensor = No
         raise ValueError("n_max must be a uint8 tensor on x's device with one entry per x")
     if offsets is None:
         offsets = ragged_offsets(nm)
-    total = int(offsets[-1].item()) if out is None else out.numel()
+    if offsets.dtype != torch.int64 or offsets.numel() != xf.numel() + 1 or \
+            offsets.device != xf.device:
+        raise ValueError("offsets must be an int64 tensor of N+1 entries on x's device")
     if out is None:
-        out = torch.empty(total, dtype=xf.dtype, device=xf.device)
+        out = torch.empty(int(offsets[-1].item()), dtype=xf.dtype, device=xf.device)
+    else:
+        if out.dtype != xf.dtype or out.device != xf.device or not out.is_contiguous():
+            raise ValueError(f"out must be a contiguous {xf.dtype} tensor on x's device")
+        # check=True already synchronises for the domain flag; the size check
+        # (one 8-byte read) keeps a short `out` from being written past its end.
+        # check=False: the caller guarantees out.numel() >= offsets[-1].
+        if check and out.numel() < int(offsets[-1].item()):
+            raise ValueError("out holds fewer values than offsets[-1]")
     dom = torch.full((1,), -1, dtype=torch.int64, device=xf.device) if check else None
     with torch.cuda.device(xf.device):
         L.check(L.load().boys_eval_ragged(_DTYPES[xf.dtype], _ptr(xf), _ptr(nm), _ptr(offsets),

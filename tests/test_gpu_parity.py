@@ -350,3 +350,16 @@ def test_ragged_host_errors():
         boys_ragged(np.abs(x), n.astype(np.int32))
     vals, off = boys_ragged(np.zeros(0), np.zeros(0, dtype=np.uint8))
     assert vals.size == 0 and off.tolist() == [0]
+
+
+def test_ragged_device_argument_checks():
+    x = torch.tensor([1.0, 2.0, 3.0], dtype=torch.float64, device="cuda")
+    n = torch.tensor([2, 0, 1], dtype=torch.uint8, device="cuda")
+    with pytest.raises(ValueError, match="fewer values"):
+        boys_ragged(x, n, out=torch.empty(5, dtype=torch.float64, device="cuda"))
+    with pytest.raises(ValueError, match="offsets must be"):
+        boys_ragged(x, n, torch.zeros(3, dtype=torch.int64, device="cuda"))
+    with pytest.raises(ValueError, match="contiguous"):
+        boys_ragged(x, n, out=torch.empty(6, dtype=torch.float32, device="cuda"))
+    vals, off = boys_ragged(x, n, out=torch.empty(7, dtype=torch.float64, device="cuda"))
+    assert off.tolist() == [0, 3, 4, 6] and vals.numel() == 7
