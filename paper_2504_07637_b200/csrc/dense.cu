@@ -189,7 +189,10 @@ static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 
 template <typename T, int n>
 static boys_status launch_soa_pair(const T* x, int64_t N, T* out, T* expx, int64_t* dom,
                                    int64_t base, cudaStream_t s) {
-  constexpr int MINB = n <= 1 ? BOYS_PAIR_MINB_SMALL : BOYS_SOA_MINB;   // two chains: 8 blocks would spill at n = 0
+#ifndef BOYS_PAIR_MINB_HIGH
+#define BOYS_PAIR_MINB_HIGH BOYS_SOA_MINB   // orders >= 11 (A/B: 3 blocks / 80 regs no better, ab45)
+#endif
+  constexpr int MINB = n <= 1 ? BOYS_PAIR_MINB_SMALL : (n >= 11 ? BOYS_PAIR_MINB_HIGH : BOYS_SOA_MINB);   // two chains: 8 blocks would spill at n = 0
   auto k = dense_soa_pair_kernel<T, n, MINB>;
   const int64_t ntiles = (N + 2 * kThreads - 1) / (2 * kThreads);
   int grid = blocks_for(k, 0, ntiles);
