@@ -469,7 +469,13 @@ static boys_status launch_ragged(const void* x, const uint8_t* nm, const int64_t
     // (order-sorted warp super-chunks were measured slower: 2.90 / 3.79 ms vs 2.42)
     // elements per lane: measured best 3 (f64: 1.95 ms vs 2.27 / 1.97 / 2.05
     // for 1 / 2 / 4) and 4 (f32: 1.14 ms vs 1.26 / 1.16 / 1.36 for 2 / 3 / 6)
-    constexpr int EPL = sizeof(T) == 8 ? 3 : 4;
+#ifndef BOYS_RAGGED_EPL64
+#define BOYS_RAGGED_EPL64 3
+#endif
+#ifndef BOYS_RAGGED_EPL32
+#define BOYS_RAGGED_EPL32 4
+#endif
+    constexpr int EPL = sizeof(T) == 8 ? BOYS_RAGGED_EPL64 : BOYS_RAGGED_EPL32;
     // (8 instead of 12 staged values per element, or a 3-blocks/SM register
     // bound, measured no better: 1.96 / 2.08 ms f64)
     // (f64, 2 elements per lane with 10 staged values each, 24 warps/SM:
