@@ -120,6 +120,15 @@ inline int ragged_grid_mult(bool f64) {
   if (v >= 1) return v;
   return f64 ? 1 : 4;
 }
+// AoS with two points per thread (dense_aos_pair_kernel): by default where the
+// double-buffered 512-point tile allows 3 blocks/SM (f64 n <= 8, every f32
+// order): f64 n=2: 168 vs 196 us, n=8: 241 vs 248 us; f32 n=8: 116 vs 144 us,
+// n=16: 197 vs 217 us at 2^24 (tools/ab/ab47.sh, ab48.sh); slower for f64
+// n >= 10 (cfg5 n=12: 1.30 vs 1.25 ms).  BOYS_AOS_PAIR=0/1 forces it off/on.
+inline bool aos_pair(bool small_tile) {
+  static int v = env_int("BOYS_AOS_PAIR", -1);
+  return v < 0 ? small_tile : v == 1;
+}
 inline int pdl() {   // BOYS_PDL=0: plain stream-serialised launches (A/B)
   static int v = env_int("BOYS_PDL", 1);
   return v;

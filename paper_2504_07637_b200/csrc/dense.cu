@@ -57,6 +57,63 @@ dense_soa_pair_kernel(const T* __restrict__ X, int64_t N, T* __restrict__ out,
   }
 }
 
+// AoS dense kernel, two points per thread (i0 + tid and i0 + 256 + tid of a
+// 512-point tile), evaluated in lockstep (eval_pair_stream); the [512][n+1]
+// tile is staged in shared memory and leaves as one bulk copy, NBUF-deep.
+// A/B variant for orders whose double-buffered tile still fits 2 blocks/SM.
+template <typename T, int n, int NBUF, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
+dense_aos_pair_kernel(const T* __restrict__ X, int64_t N, T* __restrict__ out,
+                      T* __restrict__ expx, int64_t* __restrict__ dom, int64_t index_base,
+                      bool bulk_ok) {
+  constexpr int W = n + 1;
+  constexpr int TILE = 2 * kThreads;
+  constexpr int TILE_ELEMS = TILE * W;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  T* sbase = reinterpret_cast<T*>(smem_raw);
+  const int tid = threadIdx.x;
+  const int64_t ntiles = (N + TILE - 1) / TILE;
+  pdl_wait_and_release();
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const int64_t i0 = tile * TILE;
+    const int64_t ia = i0 + tid, ib = i0 + kThreads + tid;
+    const bool ina = ia < N, inb = ib < N;
+    const T xa = ina ? ldg_nc(X + ia) : T(0);
+    const T xb = inb ? ldg_nc(X + ib) : T(0);
+    bool oka = valid_x(xa), okb = valid_x(xb);
+    if (ina && !oka) flag_domain(dom, index_base + ia);
+    if (inb && !okb) flag_domain(dom, index_base + ib);
+    oka = oka || !ina;
+    okb = okb || !inb;
+    T* buf = sbase + (it % NBUF) * TILE_ELEMS;
+    if (tid == 0) bulk_wait_read<NBUF - 1>();
+    __syncthreads();
+    T* ra = buf + tid * W;
+    T* rb = buf + (kThreads + tid) * W;
+    T ta, tb;
+    eval_pair_stream<T, n>(
+        xa, xb, oka, okb, ta, tb,
+        [&](int m, T a, T b) { ra[m] = a; rb[m] = b; },
+        [&](int j, int m, T v) { (j == 0 ? ra : rb)[m] = v; });
+    if (expx) {
+      if (ina) __stcs(expx + ia, ta);
+      if (inb) __stcs(expx + ib, tb);
+    }
+    const int64_t cnt = (N - i0) < TILE ? (N - i0) : TILE;
+    if (bulk_ok && cnt == TILE) {
+      fence_proxy_async_smem();
+      __syncthreads();
+      if (tid == 0) bulk_store(out + i0 * W, buf, TILE_ELEMS * sizeof(T));
+    } else {
+      __syncthreads();
+      T* dst = out + i0 * W;
+      for (int k = tid; k < cnt * W; k += kThreads) __stcs(dst + k, buf[k]);
+    }
+  }
+  if (tid == 0) bulk_wait_all();
+}
+
 // ---------------------------------------------------------------------------
 // dense kernel
 // ---------------------------------------------------------------------------
@@ -215,6 +272,36 @@ static boys_status launch_soa_pair(const T* x, int64_t N, T* out, T* expx, int64
   return cuda_status(cudaGetLastError());
 }
 
+template <typename T, int n>
+static boys_status launch_aos_pair(const T* x, int64_t N, T* out, T* expx, int64_t* dom,
+                                   int64_t base, cudaStream_t s) {
+  constexpr size_t tile_bytes = (size_t)2 * kThreads * (n + 1) * sizeof(T);
+  constexpr int NBUF = 2 * tile_bytes <= 110 * 1024 ? 2 : 1;
+  constexpr int MINB = NBUF * tile_bytes <= 72 * 1024 ? 3 : 2;
+  auto k = dense_aos_pair_kernel<T, n, NBUF, MINB>;
+  const size_t smem = NBUF * tile_bytes;
+  static std::atomic<uint64_t> attr_mask{0};
+  boys_status st = opt_in_smem(k, (int)smem, attr_mask);
+  if (st != BOYS_OK) return st;
+  const int64_t ntiles = (N + 2 * kThreads - 1) / (2 * kThreads);
+  const bool bulk_ok = (reinterpret_cast<uintptr_t>(out) % 16) == 0;
+  const int grid = blocks_for(k, smem, ntiles);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl() ? 1 : 0;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k, x, N, out, expx, dom, base, bulk_ok);
+  if (e != cudaSuccess) return cuda_status(e);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cuda_status(cudaGetLastError());
+}
+
 template <typename T, int n, bool AOS>
 static boys_status launch_dense_t(const T* x, int64_t N, T* out, T* expx, int64_t* dom,
                                   int64_t base, cudaStream_t s) {
@@ -228,6 +315,10 @@ static boys_status launch_dense_t(const T* x, int64_t N, T* out, T* expx, int64_
       return launch_soa_pair<T, n>(x, N, out, expx, dom, base, s);
     return launch_dense_k<T, n, false, 1, (n <= 1 ? 8 : BOYS_SOA_MINB)>(x, N, out, expx, dom, base, s);
   } else {
+    if constexpr (2 * 2 * kThreads * (n + 1) * sizeof(T) <= 110 * 1024) {
+      constexpr bool small_tile = 2 * 2 * kThreads * (n + 1) * sizeof(T) <= 72 * 1024;
+      if (aos_pair(small_tile)) return launch_aos_pair<T, n>(x, N, out, expx, dom, base, s);
+    }
     // double-buffer the AoS tile while two tiles fit in ~80 KB (n <= 18 in f64)
     constexpr bool fits2 = 2 * kThreads * (n + 1) * sizeof(T) <= 80 * 1024;
     if (fits2 && aos_nbuf() == 2)

@@ -19,6 +19,8 @@ KNOBS = [
     {"BOYS_PAIR_GRID": "1"},
     {"BOYS_SOA_TMA": "1", "BOYS_SOA_PAIR": "0"},
     {"BOYS_AOS_NBUF": "1"},
+    {"BOYS_AOS_PAIR": "1"},
+    {"BOYS_AOS_PAIR": "0"},
     {"BOYS_AOS_NBUF": "1", "BOYS_AOS_MINB": "6"},
     {"BOYS_SOA0_MINB": "6", "BOYS_SOA_PAIR": "0"},
     {"BOYS_RAGGED_EPL": "1"},
