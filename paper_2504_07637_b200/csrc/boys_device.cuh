@@ -187,6 +187,55 @@ __device__ __forceinline__ void seed_pair(const double (&x)[2], const double (&t
 // operation sequence as eval_point_stream (so the same bits); put(m, a, b)
 // receives F_m of both points at once so a SoA row takes one 16-byte store.
 // The warp-uniform shortcuts see 64 points instead of 32 (values unchanged).
+// P points per thread in lockstep (generalises eval_pair_stream; per point the
+// same operation sequence as eval_point_stream).  put(m, v[P]) gets F_m of all
+// P points; put1(j, m, v) the upward-ladder values of point j.
+template <typename T, int n, int P, typename Put, typename Put1>
+__device__ __forceinline__ void eval_multi_stream(const T (&xin)[P], const bool (&ok)[P],
+                                                  T (&tout)[P], Put&& put, Put1&& put1) {
+  using A = Ar<T>;
+  const BoysRow<T>& R = Tab<T>::row(n);
+  const T bad = A::nan();
+  T x[P], t[P], cur[P], tx[P];
+  bool below = false, up = false;
+#pragma unroll
+  for (int j = 0; j < P; ++j) {
+    x[j] = ok[j] ? xin[j] : bad;
+    t[j] = exp_neg_clamped(x[j]);
+    below = below || (ok[j] && x[j] < R.z);
+  }
+  const bool any_below = __any_sync(kFull, below);
+#pragma unroll
+  for (int j = 0; j < P; ++j) cur[j] = seed<T, n>(x[j], t[j], any_below);
+  put(n, cur);
+#pragma unroll
+  for (int j = 0; j < P; ++j) tx[j] = A::add(x[j], x[j]);
+#pragma unroll
+  for (int m = n - 1; m >= 0; --m) {
+#pragma unroll
+    for (int j = 0; j < P; ++j) cur[j] = A::mul(A::fma(tx[j], cur[j], t[j]), rinv<T>(m));
+    put(m, cur);
+  }
+#pragma unroll
+  for (int j = 0; j < P; ++j) up = up || (ok[j] && x[j] > R.x_up);
+  if (__any_sync(kFull, up)) {
+#pragma unroll
+    for (int j = 0; j < P; ++j) {
+      const bool upj = ok[j] && x[j] > R.x_up;
+      T rx = A::rcp(x[j]);
+      T f = up_first(x[j]);
+      if (upj) put1(j, 0, f);
+#pragma unroll
+      for (int m = 0; m < n; ++m) {
+        f = up_next(f, m, rx);
+        if (upj) put1(j, m + 1, f);
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < P; ++j) tout[j] = ok[j] ? t[j] : bad;
+}
+
 template <typename T, int n, typename Put, typename Put1>
 __device__ __forceinline__ void eval_pair_stream(T xa, T xb, bool oka, bool okb, T& ta_out,
                                                  T& tb_out, Put&& put, Put1&& put1) {

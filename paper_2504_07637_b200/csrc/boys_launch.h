@@ -129,6 +129,14 @@ inline bool aos_pair(bool small_tile) {
   static int v = env_int("BOYS_AOS_PAIR", -1);
   return v < 0 ? small_tile : v == 1;
 }
+// SoA with four adjacent points per thread (dense_soa_quad_kernel): default for
+// n <= 3 (f64 2^24: n=0 113 vs 123 us, n=1 122 vs 135, n=3 152 vs 167; f32
+// n <= 2 9-13% faster; n=4 neutral, n=5 slower; tools/ab/ab49.sh, ab50.sh).
+// BOYS_SOA_QUAD=0/1 forces it off/on (on: orders up to 5).
+inline bool soa_quad(int n) {
+  static int v = env_int("BOYS_SOA_QUAD", -1);
+  return v < 0 ? n <= 3 : v == 1;
+}
 inline int pdl() {   // BOYS_PDL=0: plain stream-serialised launches (A/B)
   static int v = env_int("BOYS_PDL", 1);
   return v;

@@ -57,6 +57,61 @@ dense_soa_pair_kernel(const T* __restrict__ X, int64_t N, T* __restrict__ out,
   }
 }
 
+// SoA dense kernel, four adjacent points per thread (1024-point tiles): x as
+// two 16-byte loads, every F_m row as two 16-byte streaming stores.  N % 4 == 0
+// and 16-byte aligned buffers (host checks).  A/B variant for the FP64-bound
+// small orders.
+template <typename T, int n, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
+dense_soa_quad_kernel(const T* __restrict__ X, int64_t N, T* __restrict__ out,
+                      T* __restrict__ expx, int64_t* __restrict__ dom, int64_t index_base) {
+  using V2 = typename std::conditional<sizeof(T) == 8, double2, float2>::type;
+  const int tid = threadIdx.x;
+  constexpr int TILE = 4 * kThreads;
+  const int64_t ntiles = (N + TILE - 1) / TILE;
+  pdl_wait_and_release();
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t i = tile * TILE + 4 * tid;     // N % 4 == 0 => all four in range iff i < N
+    const bool in = i < N;
+    T xv[4];
+    bool ok[4];
+    if (in) {
+      const V2 a = __ldg(reinterpret_cast<const V2*>(X + i));
+      const V2 b = __ldg(reinterpret_cast<const V2*>(X + i + 2));
+      xv[0] = a.x; xv[1] = a.y; xv[2] = b.x; xv[3] = b.y;
+    } else {
+      xv[0] = xv[1] = xv[2] = xv[3] = T(0);
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      ok[j] = valid_x(xv[j]);
+      if (in && !ok[j]) flag_domain(dom, index_base + i + j);
+      ok[j] = ok[j] || !in;
+    }
+    T* o = out + i;
+    T tv[4];
+    eval_multi_stream<T, n, 4>(
+        xv, ok, tv,
+        [&](int m, const T (&v)[4]) {
+          if (in) {
+            V2 a, b;
+            a.x = v[0]; a.y = v[1]; b.x = v[2]; b.y = v[3];
+            __stcs(reinterpret_cast<V2*>(o + (int64_t)m * N), a);
+            __stcs(reinterpret_cast<V2*>(o + (int64_t)m * N + 2), b);
+          }
+        },
+        [&](int j, int m, T v) {
+          if (in) __stcs(o + (int64_t)m * N + j, v);
+        });
+    if (expx && in) {
+      V2 a, b;
+      a.x = tv[0]; a.y = tv[1]; b.x = tv[2]; b.y = tv[3];
+      __stcs(reinterpret_cast<V2*>(expx + i), a);
+      __stcs(reinterpret_cast<V2*>(expx + i + 2), b);
+    }
+  }
+}
+
 // AoS dense kernel, two points per thread (i0 + tid and i0 + 256 + tid of a
 // 512-point tile), evaluated in lockstep (eval_pair_stream); the [512][n+1]
 // tile is staged in shared memory and leaves as one bulk copy, NBUF-deep.
@@ -272,6 +327,31 @@ static boys_status launch_soa_pair(const T* x, int64_t N, T* out, T* expx, int64
   return cuda_status(cudaGetLastError());
 }
 
+#ifndef BOYS_QUAD_MINB
+#define BOYS_QUAD_MINB 4   // 59 registers at n = 0 (3 / 2: 66 / 68, slower, ab49)
+#endif
+template <typename T, int n>
+static boys_status launch_soa_quad(const T* x, int64_t N, T* out, T* expx, int64_t* dom,
+                                   int64_t base, cudaStream_t s) {
+  auto k = dense_soa_quad_kernel<T, n, BOYS_QUAD_MINB>;
+  const int64_t ntiles = (N + 4 * kThreads - 1) / (4 * kThreads);
+  const int grid = ntiles <= ((int64_t)1 << 30) ? (int)ntiles : blocks_for(k, 0, ntiles);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl() ? 1 : 0;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k, x, N, out, expx, dom, base);
+  if (e != cudaSuccess) return cuda_status(e);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cuda_status(cudaGetLastError());
+}
+
 template <typename T, int n>
 static boys_status launch_aos_pair(const T* x, int64_t N, T* out, T* expx, int64_t* dom,
                                    int64_t base, cudaStream_t s) {
@@ -310,6 +390,10 @@ static boys_status launch_dense_t(const T* x, int64_t N, T* out, T* expx, int64_
     if (soa_tma()) return launch_dense_k<T, n, false, (fits2 ? 2 : 1), 4>(x, N, out, expx, dom, base, s);
     if constexpr (n <= 1) {          // small orders: register budget for 6 or 8 blocks/SM
       if (soa_small_minb() == 6) return launch_dense_k<T, n, false, 1, 6>(x, N, out, expx, dom, base, s);
+    }
+    if constexpr (n <= 5) {
+      if (soa_quad(n) && N % 4 == 0 && aligned16(x) && aligned16(out) && (!expx || aligned16(expx)))
+        return launch_soa_quad<T, n>(x, N, out, expx, dom, base, s);
     }
     if (soa_pair() && N % 2 == 0 && aligned16(x) && aligned16(out) && (!expx || aligned16(expx)))
       return launch_soa_pair<T, n>(x, N, out, expx, dom, base, s);
