@@ -12,6 +12,6 @@ python bench.py --steps 5 --warmup 3 --no-extras --e2e-steps 0 --cpu-seconds 0 >
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv \
     python bench.py --steps 5 --warmup 3 --no-extras --e2e-steps 0 --cpu-seconds 0 > gpurun_out/ncu_launch.log 2>&1
 timeout 120 python tools/prof_kernels.py --configs cfg3,cfg2,cfg1,cfg4,cfg4f32,cfg5 --launches 2 > gpurun_out/prof_plain.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"dense_kernel|dense_soa_pair|ragged" -s 0 -c 12 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"dense_kernel|dense_soa_pair|dense_soa_quad|dense_aos_pair|ragged" -s 0 -c 12 \
     -o gpurun_out/prof_round python tools/prof_kernels.py --configs cfg3,cfg2,cfg1,cfg4,cfg4f32,cfg5 --launches 2 > gpurun_out/ncu_full.log 2>&1
 echo done
