@@ -469,6 +469,9 @@ static boys_status launch_ragged(const void* x, const uint8_t* nm, const int64_t
     // (order-sorted warp super-chunks were measured slower: 2.90 / 3.79 ms vs 2.42)
     // elements per lane: measured best 3 (f64: 1.95 ms vs 2.27 / 1.97 / 2.05
     // for 1 / 2 / 4) and 4 (f32: 1.14 ms vs 1.26 / 1.16 / 1.36 for 2 / 3 / 6)
+#ifndef BOYS_RAGGED_CPE
+#define BOYS_RAGGED_CPE 12   // staged values per element (chunk output capacity)
+#endif
 #ifndef BOYS_RAGGED_EPL64
 #define BOYS_RAGGED_EPL64 3
 #endif
@@ -485,7 +488,7 @@ static boys_status launch_ragged(const void* x, const uint8_t* nm, const int64_t
     // f32 0.94-1.00 vs 0.94 ms, tools/ab/ab39.sh)
     boys_status st = ragged_epl() == 1
                          ? launch_chunks<T, NB, 1, NB + 1, 0>(x, nm, off, N, out, dom, s)
-                         : launch_chunks<T, NB, EPL, 12, 0>(x, nm, off, N, out, dom, s);
+                         : launch_chunks<T, NB, EPL, BOYS_RAGGED_CPE, 0>(x, nm, off, N, out, dom, s);
     if (st != BOYS_OK) return st;
   }
   g_launches.fetch_add(1, std::memory_order_relaxed);
