@@ -22,4 +22,4 @@ from .kernel import (  # noqa: F401
     ragged_offsets,
 )
 
-__version__ = "0.1.0"
+__version__ = "0.2.0"   # matches libboys (BOYS_VERSION)
