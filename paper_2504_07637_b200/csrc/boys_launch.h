@@ -137,6 +137,11 @@ inline bool soa_quad(int n) {
   static int v = env_int("BOYS_SOA_QUAD", -1);
   return v < 0 ? n <= 3 : v == 1;
 }
+// Host-buffer pipelines: elements per chunk (BOYS_HOST_CHUNK_LOG2, default 22).
+inline int64_t host_chunk() {
+  static int64_t v = int64_t(1) << env_int("BOYS_HOST_CHUNK_LOG2", 22);
+  return v;
+}
 inline int pdl() {   // BOYS_PDL=0: plain stream-serialised launches (A/B)
   static int v = env_int("BOYS_PDL", 1);
   return v;
