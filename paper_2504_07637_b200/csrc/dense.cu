@@ -1,5 +1,6 @@
-// Dense kernels (one order for the whole batch): the paired SoA kernel, the
-// one-point SoA / AoS kernel, and their launch rules.  Part of libboys.
+// Dense kernels (one order for the whole batch): the multi-point SoA kernels
+// (four / two adjacent points per thread), the paired AoS kernel, the one-point
+// SoA / AoS kernel, and their launch rules.  Part of libboys.
 #include <cuda_runtime.h>
 
 #include <atomic>
