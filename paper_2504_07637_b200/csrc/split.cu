@@ -10,12 +10,16 @@
 
 namespace boys {
 
+#ifndef BOYS_SPLIT_SOA_MINB
+#define BOYS_SPLIT_SOA_MINB 3   // SoA split: 3 resident blocks (80 regs); unbounded (134 regs, 1 block) was 2x slower (ab55)
+#endif
+
 // ---------------------------------------------------------------------------
 // split kernel (eval_with_split): F_m for m <= nbar equals a
 // dense order-nbar evaluation, F_m for m > nbar a dense order-n evaluation.
 // ---------------------------------------------------------------------------
 template <typename T, int n, bool AOS, int NBUF>
-__global__ void __launch_bounds__(kThreads, AOS ? 4 : 1)
+__global__ void __launch_bounds__(kThreads, AOS ? 4 : BOYS_SPLIT_SOA_MINB)
 split_kernel(const T* __restrict__ X, int64_t N, int nbar, T* __restrict__ out,
              int64_t* __restrict__ dom, bool bulk_ok) {
   constexpr int W = n + 1;
