@@ -142,6 +142,12 @@ inline int64_t host_chunk() {
   static int64_t v = int64_t(1) << env_int("BOYS_HOST_CHUNK_LOG2", 22);
   return v;
 }
+// Register-row AoS kernel for n = 1, 3 (dense_aos_vec_kernel); BOYS_AOS_VEC=0/1
+// forces it off/on, otherwise the per-(dtype, order) default from dense.cu.
+inline bool aos_vec(bool deflt) {
+  static int v = env_int("BOYS_AOS_VEC", -1);
+  return v < 0 ? deflt : v == 1;
+}
 inline int pdl() {   // BOYS_PDL=0: plain stream-serialised launches (A/B)
   static int v = env_int("BOYS_PDL", 1);
   return v;

@@ -113,6 +113,71 @@ dense_soa_quad_kernel(const T* __restrict__ X, int64_t N, T* __restrict__ out,
   }
 }
 
+// AoS dense kernel for rows of 2 or 4 values (n = 1, 3): P adjacent points per
+// thread, each point's row kept in registers and written straight to global
+// memory as 16-byte vectors (the thread's P rows are contiguous), no shared
+// staging.  N % P == 0 and 16-byte aligned buffers (host checks).
+template <typename T, int n, int P, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
+dense_aos_vec_kernel(const T* __restrict__ X, int64_t N, T* __restrict__ out,
+                     T* __restrict__ expx, int64_t* __restrict__ dom, int64_t index_base) {
+  using V2 = typename std::conditional<sizeof(T) == 8, double2, float2>::type;
+  constexpr int W = n + 1;
+  static_assert(W % 2 == 0, "rows of an even number of values");
+  const int tid = threadIdx.x;
+  constexpr int TILE = P * kThreads;
+  const int64_t ntiles = (N + TILE - 1) / TILE;
+  pdl_wait_and_release();
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t i = tile * TILE + P * tid;     // N % P == 0 => all P in range iff i < N
+    const bool in = i < N;
+    T xv[P], tv[P], row[P][W];
+    bool ok[P];
+#pragma unroll
+    for (int j = 0; j < P; j += 2) {
+      V2 a;
+      if (in) a = __ldg(reinterpret_cast<const V2*>(X + i + j));
+      else { a.x = T(0); a.y = T(0); }
+      xv[j] = a.x;
+      xv[j + 1] = a.y;
+    }
+#pragma unroll
+    for (int j = 0; j < P; ++j) {
+      ok[j] = valid_x(xv[j]);
+      if (in && !ok[j]) flag_domain(dom, index_base + i + j);
+      ok[j] = ok[j] || !in;
+    }
+    eval_multi_stream<T, n, P>(
+        xv, ok, tv,
+        [&](int m, const T (&v)[P]) {
+#pragma unroll
+          for (int j = 0; j < P; ++j) row[j][m] = v[j];
+        },
+        [&](int j, int m, T v) { row[j][m] = v; });
+    if (in) {
+      V2* o = reinterpret_cast<V2*>(out + i * W);
+#pragma unroll
+      for (int j = 0; j < P; ++j)
+#pragma unroll
+        for (int k = 0; k < W; k += 2) {
+          V2 v;
+          v.x = row[j][k];
+          v.y = row[j][k + 1];
+          __stcs(o + (j * W + k) / 2, v);
+        }
+      if (expx) {
+#pragma unroll
+        for (int j = 0; j < P; j += 2) {
+          V2 v;
+          v.x = tv[j];
+          v.y = tv[j + 1];
+          __stcs(reinterpret_cast<V2*>(expx + i + j), v);
+        }
+      }
+    }
+  }
+}
+
 // AoS dense kernel, two points per thread (i0 + tid and i0 + 256 + tid of a
 // 512-point tile), evaluated in lockstep (eval_pair_stream); the [512][n+1]
 // tile is staged in shared memory and leaves as one bulk copy, NBUF-deep.
@@ -328,6 +393,9 @@ static boys_status launch_soa_pair(const T* x, int64_t N, T* out, T* expx, int64
   return cuda_status(cudaGetLastError());
 }
 
+#ifndef BOYS_AOS_VEC_MINB
+#define BOYS_AOS_VEC_MINB 4
+#endif
 #ifndef BOYS_QUAD_MINB
 #define BOYS_QUAD_MINB 4   // 59 registers at n = 0 (3 / 2: 66 / 68, slower, ab49)
 #endif
@@ -336,6 +404,28 @@ static boys_status launch_soa_quad(const T* x, int64_t N, T* out, T* expx, int64
                                    int64_t base, cudaStream_t s) {
   auto k = dense_soa_quad_kernel<T, n, BOYS_QUAD_MINB>;
   const int64_t ntiles = (N + 4 * kThreads - 1) / (4 * kThreads);
+  const int grid = ntiles <= ((int64_t)1 << 30) ? (int)ntiles : blocks_for(k, 0, ntiles);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl() ? 1 : 0;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k, x, N, out, expx, dom, base);
+  if (e != cudaSuccess) return cuda_status(e);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cuda_status(cudaGetLastError());
+}
+
+template <typename T, int n, int P>
+static boys_status launch_aos_vec(const T* x, int64_t N, T* out, T* expx, int64_t* dom,
+                                  int64_t base, cudaStream_t s) {
+  auto k = dense_aos_vec_kernel<T, n, P, BOYS_AOS_VEC_MINB>;
+  const int64_t ntiles = (N + P * kThreads - 1) / (P * kThreads);
   const int grid = ntiles <= ((int64_t)1 << 30) ? (int)ntiles : blocks_for(k, 0, ntiles);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -400,6 +490,17 @@ static boys_status launch_dense_t(const T* x, int64_t N, T* out, T* expx, int64_
       return launch_soa_pair<T, n>(x, N, out, expx, dom, base, s);
     return launch_dense_k<T, n, false, 1, (n <= 1 ? 8 : BOYS_SOA_MINB)>(x, N, out, expx, dom, base, s);
   } else {
+    if constexpr (n == 1 || n == 3) {
+      // register rows + direct 16-byte stores: default for n = 1 (4 points per
+      // thread) and f32 n = 3 (2 points); f64 n = 3 keeps the staged pair
+      // kernel (ab56: n=1 f64 128.6 vs 158.2 us, f32 63.4 vs 91.2 us; f32 n=3
+      // 88.1 vs 97.8 us; f64 n=3 180 vs 173 us)
+      constexpr int P = n == 1 ? 4 : 2;
+      constexpr bool deflt = n == 1 || sizeof(T) == 4;
+      if (aos_vec(deflt) && N % P == 0 && aligned16(x) && aligned16(out) &&
+          (!expx || aligned16(expx)))
+        return launch_aos_vec<T, n, P>(x, N, out, expx, dom, base, s);
+    }
     if constexpr (2 * 2 * kThreads * (n + 1) * sizeof(T) <= 110 * 1024) {
       constexpr bool small_tile = 2 * 2 * kThreads * (n + 1) * sizeof(T) <= 72 * 1024;
       if (aos_pair(small_tile)) return launch_aos_pair<T, n>(x, N, out, expx, dom, base, s);

@@ -23,6 +23,8 @@ KNOBS = [
     {"BOYS_AOS_PAIR": "0"},
     {"BOYS_SOA_QUAD": "1"},
     {"BOYS_SOA_QUAD": "0"},
+    {"BOYS_AOS_VEC": "1"},
+    {"BOYS_AOS_VEC": "0"},
     {"BOYS_AOS_NBUF": "1", "BOYS_AOS_MINB": "6"},
     {"BOYS_SOA0_MINB": "6", "BOYS_SOA_PAIR": "0"},
     {"BOYS_RAGGED_EPL": "1"},
