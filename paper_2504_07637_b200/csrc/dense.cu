@@ -123,7 +123,7 @@ dense_aos_vec_kernel(const T* __restrict__ X, int64_t N, T* __restrict__ out,
                      T* __restrict__ expx, int64_t* __restrict__ dom, int64_t index_base) {
   using V2 = typename std::conditional<sizeof(T) == 8, double2, float2>::type;
   constexpr int W = n + 1;
-  static_assert(W % 2 == 0, "rows of an even number of values");
+  static_assert((P * W) % 2 == 0 && P % 2 == 0, "P rows of W values: whole 16-byte vectors");
   const int tid = threadIdx.x;
   constexpr int TILE = P * kThreads;
   const int64_t ntiles = (N + TILE - 1) / TILE;
@@ -155,16 +155,16 @@ dense_aos_vec_kernel(const T* __restrict__ X, int64_t N, T* __restrict__ out,
         },
         [&](int j, int m, T v) { row[j][m] = v; });
     if (in) {
+      // the thread's P rows are P*W contiguous values starting at a 16-byte
+      // boundary (i is a multiple of P, P even): whole 16-byte vectors
       V2* o = reinterpret_cast<V2*>(out + i * W);
 #pragma unroll
-      for (int j = 0; j < P; ++j)
-#pragma unroll
-        for (int k = 0; k < W; k += 2) {
-          V2 v;
-          v.x = row[j][k];
-          v.y = row[j][k + 1];
-          __stcs(o + (j * W + k) / 2, v);
-        }
+      for (int f = 0; f < P * W; f += 2) {
+        V2 v;
+        v.x = row[f / W][f % W];
+        v.y = row[(f + 1) / W][(f + 1) % W];
+        __stcs(o + f / 2, v);
+      }
       if (expx) {
 #pragma unroll
         for (int j = 0; j < P; j += 2) {
@@ -393,6 +393,9 @@ static boys_status launch_soa_pair(const T* x, int64_t N, T* out, T* expx, int64
   return cuda_status(cudaGetLastError());
 }
 
+#ifndef BOYS_AOS_VEC_P
+#define BOYS_AOS_VEC_P 0     // A/B override of the register-row kernel's points per thread
+#endif
 #ifndef BOYS_AOS_VEC_MINB
 #define BOYS_AOS_VEC_MINB 4
 #endif
@@ -490,13 +493,14 @@ static boys_status launch_dense_t(const T* x, int64_t N, T* out, T* expx, int64_
       return launch_soa_pair<T, n>(x, N, out, expx, dom, base, s);
     return launch_dense_k<T, n, false, 1, (n <= 1 ? 8 : BOYS_SOA_MINB)>(x, N, out, expx, dom, base, s);
   } else {
-    if constexpr (n == 1 || n == 3) {
-      // register rows + direct 16-byte stores: default for n = 1 (4 points per
-      // thread) and f32 n = 3 (2 points); f64 n = 3 keeps the staged pair
-      // kernel (ab56: n=1 f64 128.6 vs 158.2 us, f32 63.4 vs 91.2 us; f32 n=3
-      // 88.1 vs 97.8 us; f64 n=3 180 vs 173 us)
-      constexpr int P = n == 1 ? 4 : 2;
-      constexpr bool deflt = n == 1 || sizeof(T) == 4;
+    if constexpr (n >= 1 && n <= 6) {
+      // register rows + direct 16-byte stores: default for n = 1, 2 and f32
+      // n = 3; the staged kernels win from n = 4 (f64 from n = 3).  ab56/ab57,
+      // 2^24: n=1 f64 128.6 vs 158.2 us, f32 63.4 vs 91.2; n=2 f64 149.2 vs
+      // 168.1, f32 82.9 vs 96.2; f32 n=3 88.1 vs 97.8; f64 n=3 180 vs 173.
+      constexpr int P = BOYS_AOS_VEC_P > 0 ? BOYS_AOS_VEC_P
+                        : (n == 1 || (n == 2 && sizeof(T) == 8)) ? 4 : 2;
+      constexpr bool deflt = n <= 2 || (n == 3 && sizeof(T) == 4);
       if (aos_vec(deflt) && N % P == 0 && aligned16(x) && aligned16(out) &&
           (!expx || aligned16(expx)))
         return launch_aos_vec<T, n, P>(x, N, out, expx, dom, base, s);
