@@ -94,13 +94,22 @@ def test_config_inputs_bit_exact(oracle, cfg):
     assert_parity(got, ref, cfg)
 
 
-@pytest.mark.parametrize("N", [0, 1, 2, 255, 256, 257, 1000, 65537])
+@pytest.mark.parametrize("N", [0, 1, 2, 4, 255, 256, 257, 514, 1000, 1028, 2048, 65537, 65540])
 def test_sizes_and_tails(oracle, N):
-    for n, layout in ((16, "aos"), (12, "aos"), (8, "soa"), (3, "aos")):
+    # every dense kernel family: SoA quad (n <= 3, N % 4 == 0), SoA pair (N even),
+    # SoA one point (odd N), AoS register rows (n = 1, 2), AoS pair (n <= 8),
+    # AoS one point (n >= 9); f32 for the f32-only defaults
+    for n, layout in ((16, "aos"), (12, "aos"), (8, "soa"), (3, "aos"), (0, "soa"), (1, "soa"),
+                      (3, "soa"), (1, "aos"), (2, "aos"), (6, "aos")):
         x = np.abs(np.random.default_rng(N).standard_normal(N)) * 30
         got = boys(n, torch.from_numpy(x).cuda(), layout=layout).cpu().numpy()
         ref, _ = oracle.dense(n, x, layout)
         assert_parity(got, ref, f"N={N} n={n} {layout}")
+    for n, layout in ((3, "aos"), (2, "aos"), (1, "soa"), (8, "aos")):
+        x = (np.abs(np.random.default_rng(N + 1).standard_normal(N)) * 30).astype(np.float32)
+        got = boys(n, torch.from_numpy(x).cuda(), layout=layout).cpu().numpy()
+        ref, _ = oracle.dense(n, x, layout)
+        assert_parity(got, ref, f"f32 N={N} n={n} {layout}")
 
 
 def test_unaligned_out_falls_back(oracle):
