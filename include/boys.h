@@ -111,6 +111,39 @@ boys_status boys_eval_ragged_host(boys_dtype dtype, const void* x_host, const ui
                                   int64_t N, void* out_host, int64_t out_capacity,
                                   int64_t* first_bad);
 
+/* ---- coefficient tables (eval_batch(req, KernelTable),
+ * eval_with_split(n, n_bar, x, table), table loading from the coeffs file) ----
+ * The compiled-in tables serve boys_eval_dense / _split / _ragged.  A caller
+ * holding a different KernelTable (a refit, another dataset file) uploads it
+ * once and evaluates through the *_table entries; values are bit-identical to
+ * the CPU restatement loaded with that dataset.  Row layout: BoysRow<T> of
+ * csrc/boys_eval.cuh (q0 q1 q2 c z x_up, uq[8][2], ul[2], vq[8][2], vl[2] in
+ * the dtype, then int32 cnt[4]), boys_table_row_bytes(dtype) bytes per order. */
+typedef struct boys_table boys_table;
+
+/* SHA-256 (hex) of the compiled table's packed rows (coeffs.table_checksum). */
+const char* boys_table_checksum(boys_dtype dtype);
+size_t boys_table_row_bytes(boys_dtype dtype);
+/* Upload rows for orders 0..n_rows-1 to the current device (synchronous). */
+boys_status boys_table_create(boys_dtype dtype, const void* rows_host, int n_rows,
+                              size_t row_bytes, boys_table** out);
+boys_status boys_table_destroy(boys_table* table);
+int boys_table_max_order(const boys_table* table);
+boys_status boys_eval_dense_table(const boys_table* table, int n_max, const void* x_dev,
+                                  int64_t N, void* out_dev, boys_layout layout, void* expx_dev,
+                                  int64_t* dom_dev, void* stream);
+boys_status boys_eval_split_table(const boys_table* table, int n, int n_bar, const void* x_dev,
+                                  int64_t N, void* out_dev, boys_layout layout,
+                                  int64_t* dom_dev, void* stream);
+
+/* Per-shard error statistic (the multi-GPU path's only reduction):
+ * *err_dev = max(*err_dev, max_j |(vals[pos_j] - hi_j) - lo_j| / |hi_j|) over
+ * j < K, gold_dev = K (hi, lo) double-double reference pairs; |hi_j| below the
+ * dtype's smallest normal contributes 0, NaN contributes +inf.  Stream-ordered,
+ * one launch; the caller initialises *err_dev (0.0) and gathers it across ranks. */
+boys_status boys_shard_error(boys_dtype dtype, const void* vals_dev, const int64_t* pos_dev,
+                             const double* gold_dev, int64_t K, double* err_dev, void* stream);
+
 /* Number of kernel launches issued by this library in this process. */
 int64_t boys_launch_count(void);
 

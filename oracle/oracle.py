@@ -84,15 +84,19 @@ def lib():
     return _lib
 
 
-def table(dtype):
+def table(dtype, path=None):
+    """Oracle table for dtype: the shipped dataset, or the dataset file `path`
+    (the oracle's own parser; used to check the uploaded-table path)."""
     dtype = np.dtype(dtype)
-    if dtype not in _tables:
+    key = (dtype, str(path) if path else None)
+    if key not in _tables:
         prof = "single24" if dtype == np.float32 else "double53"
-        t = lib().boys_oracle_load(str(DATA / f"boys_{prof}.dat").encode())
+        src = str(path) if path else str(DATA / f"boys_{prof}.dat")
+        t = lib().boys_oracle_load(src.encode())
         if not t:
-            raise RuntimeError(f"oracle could not parse the {prof} dataset")
-        _tables[dtype] = t
-    return _tables[dtype]
+            raise RuntimeError(f"oracle could not parse the dataset {src}")
+        _tables[key] = t
+    return _tables[key]
 
 
 def max_order(dtype) -> int:
@@ -103,16 +107,17 @@ def _ptr(a):
     return a.ctypes.data_as(C.c_void_p)
 
 
-def dense(n: int, x, layout: str = "soa", expx: bool = False):
+def dense(n: int, x, layout: str = "soa", expx: bool = False, table_path=None):
     """F_0..F_n for every x (dtype float64 or float32).  Returns
-    (values, first_bad[, expx]); values [n+1][N] (soa) or [N][n+1] (aos)."""
+    (values, first_bad[, expx]); values [n+1][N] (soa) or [N][n+1] (aos).
+    table_path: evaluate with that dataset file instead of the shipped one."""
     x = np.ascontiguousarray(x)
     assert x.dtype in (np.float64, np.float32)
     N = x.size
     shape = (n + 1, N) if layout == "soa" else (N, n + 1)
     out = np.empty(shape, dtype=x.dtype)
     ex = np.empty(N, dtype=x.dtype) if expx else None
-    bad = lib().boys_oracle_dense(table(x.dtype), n, _ptr(x), N, _ptr(out),
+    bad = lib().boys_oracle_dense(table(x.dtype, table_path), n, _ptr(x), N, _ptr(out),
                                   0 if layout == "soa" else 1, _ptr(ex) if expx else None)
     return (out, bad, ex) if expx else (out, bad)
 
@@ -134,11 +139,11 @@ def ragged(x, nmax):
     return out, off, bad
 
 
-def split(n: int, nbar: int, x, layout: str = "soa"):
+def split(n: int, nbar: int, x, layout: str = "soa", table_path=None):
     x = np.ascontiguousarray(x)
     N = x.size
     out = np.empty((n + 1, N) if layout == "soa" else (N, n + 1), dtype=x.dtype)
-    bad = lib().boys_oracle_split(table(x.dtype), n, nbar, _ptr(x), N, _ptr(out),
+    bad = lib().boys_oracle_split(table(x.dtype, table_path), n, nbar, _ptr(x), N, _ptr(out),
                                   0 if layout == "soa" else 1)
     return out, bad
 

@@ -22,6 +22,8 @@ EXPORTS = (
     "boys_max_order", "boys_version", "boys_eval_dense", "boys_eval_ragged",
     "boys_ragged_offsets", "boys_eval_split", "boys_domain_result", "boys_eval_dense_host", "boys_eval_ragged_host",
     "boys_launch_count", "boys_status_str", "boys_last_cuda_error",
+    "boys_table_checksum", "boys_table_row_bytes", "boys_table_create", "boys_table_destroy",
+    "boys_table_max_order", "boys_eval_dense_table", "boys_eval_split_table", "boys_shard_error",
 )
 
 _lock = threading.Lock()
@@ -68,6 +70,22 @@ def load(build_if_missing: bool = True) -> C.CDLL:
         L.boys_eval_dense_host.argtypes = [i32, i32, vp, i64, vp, i32, C.POINTER(i64)]
         L.boys_eval_ragged_host.restype = i32
         L.boys_eval_ragged_host.argtypes = [i32, vp, vp, i64, vp, i64, C.POINTER(i64)]
+        L.boys_table_checksum.restype = C.c_char_p
+        L.boys_table_checksum.argtypes = [i32]
+        L.boys_table_row_bytes.restype = C.c_size_t
+        L.boys_table_row_bytes.argtypes = [i32]
+        L.boys_table_create.restype = i32
+        L.boys_table_create.argtypes = [i32, vp, i32, C.c_size_t, C.POINTER(vp)]
+        L.boys_table_destroy.restype = i32
+        L.boys_table_destroy.argtypes = [vp]
+        L.boys_table_max_order.restype = i32
+        L.boys_table_max_order.argtypes = [vp]
+        L.boys_eval_dense_table.restype = i32
+        L.boys_eval_dense_table.argtypes = [vp, i32, vp, i64, vp, i32, vp, vp, vp]
+        L.boys_eval_split_table.restype = i32
+        L.boys_eval_split_table.argtypes = [vp, i32, i32, vp, i64, vp, i32, vp, vp]
+        L.boys_shard_error.restype = i32
+        L.boys_shard_error.argtypes = [i32, vp, vp, vp, i64, vp, vp]
         L.boys_launch_count.restype = i64
         L.boys_status_str.restype = C.c_char_p
         L.boys_status_str.argtypes = [i32]

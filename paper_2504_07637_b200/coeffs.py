@@ -275,6 +275,27 @@ def build_kernel_table(ds: Dataset) -> KernelTable:
     return KernelTable(profile=ds.profile, orders=orders, counts=counts, rows=rows)
 
 
+def pack_rows(kt: KernelTable) -> bytes:
+    """The table as the kernels hold it: one ``BoysRow<T>`` per order
+    (csrc/boys_eval.cuh field order -- q0 q1 q2 c z x_up, uq[8][2], ul[2],
+    vq[8][2], vl[2] in T, then cnt[4] int32; no padding for either T).
+    Uploaded verbatim by ``boys_table_create``; its SHA-256 identifies a table."""
+    fmt = "<42f4i" if kt.profile == "single24" else "<42d4i"
+    out = []
+    for row, cnt in zip(kt.rows, kt.counts):
+        vals = [row[k] for k in ("q0", "q1", "q2", "c", "z", "x_up")]
+        vals += [v for pair in row["uq"] for v in pair] + list(row["ul"])
+        vals += [v for pair in row["vq"] for v in pair] + list(row["vl"])
+        out.append(struct.pack(fmt, *vals, *cnt))
+    return b"".join(out)
+
+
+def table_checksum(kt: KernelTable) -> str:
+    """SHA-256 of ``pack_rows(kt)`` (libboys exports the compiled table's
+    digest as ``boys_table_checksum``)."""
+    return hashlib.sha256(pack_rows(kt)).hexdigest()
+
+
 def _lit(v: float, single: bool) -> str:
     s = float(v).hex()
     return s + ("f" if single else "")
@@ -297,6 +318,7 @@ def gen_header(tables: list) -> str:
         tag = "F32" if single else "F64"
         nmax = kt.max_order
         out.append(f"#define BOYS_{tag}_MAX_ORDER {nmax}")
+        out.append(f'#define BOYS_{tag}_TABLE_SHA256 "{table_checksum(kt)}"')
         out.append(f"// counts per order: {{u quads, u lins, v quads, v lins}}")
         out.append(f"__host__ __device__ constexpr int boys_shape_{tag.lower()}(int n, int k) {{")
         out.append(f"  constexpr int s[{nmax + 1}][4] = {{")

@@ -181,6 +181,10 @@ boys_status boys_eval_ragged(boys_dtype dtype, const void* x_dev, const uint8_t*
   if (N < 0) return BOYS_E_ARG;
   if (N == 0) return BOYS_OK;
   if (!x_dev || !nmax_dev || !offsets_dev || !out_dev) return BOYS_E_ARG;
+  // element alignment (the kernel derives the 16-byte phase from the address)
+  if ((reinterpret_cast<uintptr_t>(x_dev) | reinterpret_cast<uintptr_t>(out_dev)) % dsize(dtype) ||
+      reinterpret_cast<uintptr_t>(offsets_dev) % sizeof(int64_t))
+    return BOYS_E_ALIGN;
   return eval_ragged_base(dtype, x_dev, nmax_dev, offsets_dev, N, out_dev, dom_dev,
                           (cudaStream_t)stream);
 }
@@ -189,6 +193,13 @@ boys_status boys_ragged_offsets(const uint8_t* nmax_dev, int64_t N, int64_t* off
                                 void* stream) {
   if (N < 0 || !offsets_dev || (N > 0 && !nmax_dev)) return BOYS_E_ARG;
   return ragged_offsets_base(nmax_dev, N, offsets_dev, (cudaStream_t)stream);
+}
+
+boys_status boys_shard_error(boys_dtype dtype, const void* vals_dev, const int64_t* pos_dev,
+                             const double* gold_dev, int64_t K, double* err_dev, void* stream) {
+  if (dtype != BOYS_F64 && dtype != BOYS_F32) return BOYS_E_DTYPE;
+  if (K < 0 || !err_dev || (K > 0 && (!vals_dev || !pos_dev || !gold_dev))) return BOYS_E_ARG;
+  return shard_error_base(dtype, vals_dev, pos_dev, gold_dev, K, err_dev, (cudaStream_t)stream);
 }
 
 boys_status boys_domain_result(const int64_t* dom_dev, int64_t* first_bad, void* stream) {

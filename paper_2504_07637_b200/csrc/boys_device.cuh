@@ -315,6 +315,11 @@ struct SmemRows {
   __device__ __forceinline__ const BoysRow<T>& operator()(int n) const { return p[n]; }
 };
 template <typename T>
+struct PtrRows {   // rows in global memory (a table uploaded at run time)
+  const BoysRow<T>* __restrict__ p;
+  __device__ __forceinline__ const BoysRow<T>& operator()(int n) const { return p[n]; }
+};
+template <typename T>
 struct ConstRows {
   __device__ __forceinline__ const BoysRow<T>& operator()(int n) const { return Tab<T>::row(n); }
 };
@@ -456,8 +461,8 @@ __device__ __forceinline__ T factored_uniform(T x, const T (*q)[2], const T* l, 
 // (split kernel): uniform loop bounds instead of per-lane selects.  Invalid
 // lanes evaluate x = 0 at that order and output NaN, as in eval_point_rt.
 template <typename T, int NB, typename Rows, typename Put>
-__device__ __forceinline__ void eval_point_uniform(T x_in, bool ok, int n, const Rows& rows,
-                                                   Put&& put) {
+__device__ __forceinline__ T eval_point_uniform(T x_in, bool ok, int n, const Rows& rows,
+                                                Put&& put) {
   using A = Ar<T>;
   constexpr int MQ = MaxShape<T>::Q(), ML = MaxShape<T>::L();
   T x = ok ? x_in : T(0);
@@ -480,6 +485,7 @@ __device__ __forceinline__ void eval_point_uniform(T x_in, bool ok, int n, const
   tail_rt<T, NB>(x, y, t, n, ok, n, rows, [&](int m, T v, bool on) {
     if (on) put(m, v);
   });
+  return ok ? t : A::nan();
 }
 
 // Complete run-time-order evaluation (split kernel; ragged fallback tiles).

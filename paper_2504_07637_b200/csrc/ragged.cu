@@ -208,7 +208,8 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
     }
     // staging position matches the global 16-byte phase of the chunk range
     constexpr int Q = 16 / sizeof(T);
-    const int shift = (int)(base & (Q - 1));
+    // (from the address: `out` need only be element-aligned)
+    const int shift = (int)((reinterpret_cast<uintptr_t>(out + base) / sizeof(T)) & (Q - 1));
     // the previous chunk's bulk store must have finished reading the slot
     if (lane == 0) bulk_wait_read<0>();
     __syncwarp();
@@ -250,41 +251,11 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
       const int wmax = __reduce_max_sync(kFull, (unsigned)wmax_l);
       const int bits = 32 - __clz(wmax | 1);
       T r[EPL], sr[EPL];
-#if BOYS_FAST_CR
-      // correctly rounded 1/x and sqrt through the branch-free fast paths for
-      // all EPL elements at once (interleaved chains); the rare slow-path
-      // lanes (x near 0 / the exponent limits, NaN) recompute with the intrinsics
-      {
-        bool slow = false;
-#pragma unroll
-        for (int e = 0; e < EPL; ++e) {
-          bool s1;
-          r[e] = A::rcp_fast(xs[e], s1);
-          slow = slow || s1;
-        }
-        if (__any_sync(kFull, slow)) {
-#pragma unroll
-          for (int e = 0; e < EPL; ++e) r[e] = A::rcp(xs[e]);
-        }
-        slow = false;
-#pragma unroll
-        for (int e = 0; e < EPL; ++e) {
-          bool s2;
-          sr[e] = A::sqrt_fast(r[e], s2);
-          slow = slow || s2;
-        }
-        if (__any_sync(kFull, slow)) {
-#pragma unroll
-          for (int e = 0; e < EPL; ++e) sr[e] = A::sqrt(r[e]);
-        }
-      }
-#else
 #pragma unroll
       for (int e = 0; e < EPL; ++e) {
         r[e] = A::rcp(xs[e]);
         sr[e] = A::sqrt(r[e]);
       }
-#endif
 #pragma unroll
       for (int e = 0; e < EPL; ++e) {
         const T cn = zc[e].c;
@@ -382,64 +353,142 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
 // 1.00 ms) and was removed; it is in the history up to commit 50d605b.)
 
 // ---------------------------------------------------------------------------
-// ragged offsets: exclusive prefix sum of (n_i + 1), single-pass per block +
-// a tiny second pass over block totals (decoupled; two launches)
+// ragged offsets: exclusive prefix sum of (n_i + 1), O(N) in three launches
+// and no workspace.  The output array itself holds the block totals:
+//   1. block b sums its tile and stores the total at OFF[min((b+1) TILE, N)]
+//      -- a slot that pass 3 (block b+1) or pass 2 (OFF[N]) overwrites;
+//   2. one block scans the nblk totals (strided reads) and writes block b's
+//      exclusive prefix to OFF[b TILE] and the grand total to OFF[N];
+//   3. block b scans its tile from that prefix (shared-memory transpose, so
+//      the int64 stores leave coalesced).
+// Traffic: n_max read twice + offsets written once.
 // ---------------------------------------------------------------------------
-__global__ void offsets_block_kernel(const uint8_t* __restrict__ NM, int64_t N,
-                                     int64_t* __restrict__ OFF, int64_t* __restrict__ blk) {
-  __shared__ int64_t s[kThreads];
-  const int64_t per = 8;
-  const int64_t b0 = (int64_t)blockIdx.x * kThreads * per;
-  int64_t loc[8];
-  int64_t acc = 0;
-  for (int k = 0; k < per; ++k) {
-    int64_t i = b0 + threadIdx.x * per + k;
-    loc[k] = acc;
-    acc += (i < N) ? (int64_t)NM[i] + 1 : 0;
-  }
-  s[threadIdx.x] = acc;
-  __syncthreads();
-  for (int d = 1; d < kThreads; d <<= 1) {
-    int64_t v = threadIdx.x >= d ? s[threadIdx.x - d] : 0;
-    __syncthreads();
-    s[threadIdx.x] += v;
-    __syncthreads();
-  }
-  int64_t excl = s[threadIdx.x] - acc;
-  for (int k = 0; k < per; ++k) {
-    int64_t i = b0 + threadIdx.x * per + k;
-    if (i < N) OFF[i] = excl + loc[k];
-  }
-  if (threadIdx.x == kThreads - 1) blk[blockIdx.x] = s[threadIdx.x];
-}
+constexpr int kScanPer = 16;                         // elements per thread
+constexpr int kScanTile = kThreads * kScanPer;       // 4096 elements per block
 
-__global__ void offsets_fix_kernel(int64_t N, int64_t nblk, int64_t* __restrict__ OFF,
-                                   const int64_t* __restrict__ blk) {
-  // every block redundantly scans the block totals it needs (nblk is small)
-  __shared__ int64_t add;
-  const int64_t per = 8;
-  const int64_t b = blockIdx.x;
-  if (threadIdx.x == 0) {
-    int64_t a = 0;
-    for (int64_t k = 0; k < b; ++k) a += blk[k];
-    add = a;
-  }
-  __syncthreads();
-  const int64_t b0 = b * kThreads * per;
-  for (int k = 0; k < per; ++k) {
-    int64_t i = b0 + threadIdx.x * per + k;
-    if (i < N) OFF[i] += add;
-  }
-  if (b == nblk - 1 && threadIdx.x == 0) {
-    int64_t a = 0;
-    for (int64_t k = 0; k < nblk; ++k) a += blk[k];
-    OFF[N] = a;
+// the thread's 16 consecutive orders (16-byte vector load when aligned)
+__device__ __forceinline__ void scan_load16(const uint8_t* __restrict__ NM, int64_t N, int64_t i0,
+                                            bool vec, int (&v)[kScanPer]) {
+  if (vec && i0 + kScanPer <= N) {
+    const uint4 q = __ldg(reinterpret_cast<const uint4*>(NM + i0));
+    const unsigned w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int k = 0; k < kScanPer; ++k) v[k] = (int)((w[k >> 2] >> (8 * (k & 3))) & 0xffu) + 1;
+  } else {
+#pragma unroll
+    for (int k = 0; k < kScanPer; ++k) v[k] = (i0 + k < N) ? (int)NM[i0 + k] + 1 : 0;
   }
 }
 
-inline int ragged_epl() {   // BOYS_RAGGED_EPL=1: one element per lane (A/B)
-  static int v = env_int("BOYS_RAGGED_EPL", 0);
-  return v;
+// block-wide exclusive scan of one int64 per thread (warp shuffles + 8 warp sums)
+__device__ __forceinline__ int64_t block_excl_scan(int64_t v, int64_t* s_warp, int64_t& total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int64_t inc = v;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int64_t o = __shfl_up_sync(kFull, inc, d);
+    if (lane >= d) inc += o;
+  }
+  if (lane == 31) s_warp[wid] = inc;
+  __syncthreads();
+  int64_t wpre = 0;
+  total = 0;
+#pragma unroll
+  for (int w = 0; w < kThreads / 32; ++w) {
+    const int64_t t = s_warp[w];
+    wpre += w < wid ? t : 0;
+    total += t;
+  }
+  return wpre + inc - v;
+}
+
+__global__ void __launch_bounds__(kThreads)
+offsets_totals_kernel(const uint8_t* __restrict__ NM, int64_t N, int64_t* __restrict__ OFF,
+                      bool vec) {
+  __shared__ int64_t s_warp[kThreads / 32];
+  const int64_t b0 = (int64_t)blockIdx.x * kScanTile;
+  int v[kScanPer];
+  scan_load16(NM, N, b0 + (int64_t)threadIdx.x * kScanPer, vec, v);
+  int sum = 0;
+#pragma unroll
+  for (int k = 0; k < kScanPer; ++k) sum += v[k];
+  int64_t total;
+  block_excl_scan(sum, s_warp, total);
+  if (threadIdx.x == 0) OFF[min(b0 + kScanTile, N)] = total;
+}
+
+// one block: exclusive prefix of the block totals, in place
+__global__ void __launch_bounds__(1024)
+offsets_blocks_kernel(int64_t N, int64_t nblk, int64_t* __restrict__ OFF) {
+  __shared__ int64_t s_warp[32];
+  __shared__ int64_t s_carry;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_carry = 0;
+  __syncthreads();
+  // rounds of 1024 * 8 totals: thread t takes 8 consecutive blocks
+  constexpr int PER = 8;
+  for (int64_t r0 = 0; r0 < nblk; r0 += 1024 * PER) {
+    const int64_t b0 = r0 + (int64_t)threadIdx.x * PER;
+    int64_t t[PER], sum = 0;
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int64_t b = b0 + k;
+      t[k] = b < nblk ? OFF[min((b + 1) * kScanTile, N)] : 0;
+      sum += t[k];
+    }
+    int64_t inc = sum;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int64_t o = __shfl_up_sync(kFull, inc, d);
+      if (lane >= d) inc += o;
+    }
+    if (lane == 31) s_warp[wid] = inc;
+    __syncthreads();                       // every total of this round has been read
+    int64_t wpre = 0, total = 0;
+    for (int w = 0; w < 32; ++w) {
+      const int64_t s = s_warp[w];
+      wpre += w < wid ? s : 0;
+      total += s;
+    }
+    int64_t p = s_carry + wpre + inc - sum;
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int64_t b = b0 + k;
+      if (b < nblk) OFF[b * kScanTile] = p;     // b = 0 writes OFF[0] = 0
+      p += t[k];
+    }
+    __syncthreads();                       // s_warp / s_carry reuse
+    if (threadIdx.x == 0) s_carry += total;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) OFF[N] = s_carry;
+}
+
+__global__ void __launch_bounds__(kThreads)
+offsets_tiles_kernel(const uint8_t* __restrict__ NM, int64_t N, int64_t* __restrict__ OFF,
+                     bool vec) {
+  __shared__ int64_t s_warp[kThreads / 32];
+  constexpr int RS = kScanPer + 1;           // padded row: conflict-free row writes
+  __shared__ int64_t s_out[kThreads * RS];
+  const int64_t b0 = (int64_t)blockIdx.x * kScanTile;
+  const int64_t prefix = OFF[b0];            // written by pass 2 (b0 < N always)
+  int v[kScanPer];
+  scan_load16(NM, N, b0 + (int64_t)threadIdx.x * kScanPer, vec, v);
+  int sum = 0;
+#pragma unroll
+  for (int k = 0; k < kScanPer; ++k) sum += v[k];
+  int64_t total;
+  int64_t p = prefix + block_excl_scan(sum, s_warp, total);
+  // transpose through shared memory so the int64 stores leave coalesced
+#pragma unroll
+  for (int k = 0; k < kScanPer; ++k) {
+    s_out[threadIdx.x * RS + k] = p;
+    p += v[k];
+  }
+  __syncthreads();
+  const int cnt = (int)min((int64_t)kScanTile, N - b0);
+  for (int k = threadIdx.x; k < cnt; k += kThreads)
+    OFF[b0 + k] = s_out[(k / kScanPer) * RS + (k % kScanPer)];
 }
 
 template <typename T, int NB, int EPL, int CPE, int MINB, int WT = kThreads>
@@ -486,9 +535,7 @@ static boys_status launch_ragged(const void* x, const uint8_t* nm, const int64_t
     // (128-thread blocks, also with a 96-register bound and 8 staged values per
     // element for 20 resident warps, measured slower: f64 1.84-2.36 vs 1.78 ms,
     // f32 0.94-1.00 vs 0.94 ms, tools/ab/ab39.sh)
-    boys_status st = ragged_epl() == 1
-                         ? launch_chunks<T, NB, 1, NB + 1, 0>(x, nm, off, N, out, dom, s)
-                         : launch_chunks<T, NB, EPL, BOYS_RAGGED_CPE, 0>(x, nm, off, N, out, dom, s);
+    boys_status st = launch_chunks<T, NB, EPL, BOYS_RAGGED_CPE, 0>(x, nm, off, N, out, dom, s);
     if (st != BOYS_OK) return st;
   }
   g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -505,17 +552,14 @@ boys_status eval_ragged_base(boys_dtype dtype, const void* x, const uint8_t* nm,
 boys_status ragged_offsets_base(const uint8_t* nmax_dev, int64_t N, int64_t* offsets_dev,
                                 cudaStream_t s) {
   if (N == 0) return cuda_status(cudaMemsetAsync(offsets_dev, 0, sizeof(int64_t), s));
-  const int64_t per_blk = (int64_t)kThreads * 8;
-  const int64_t nblk = (N + per_blk - 1) / per_blk;
-  int64_t* blk = nullptr;
-  cudaError_t e = cudaMallocAsync(&blk, nblk * sizeof(int64_t), s);
-  if (e != cudaSuccess) return cuda_status(e);
-  offsets_block_kernel<<<(unsigned)nblk, kThreads, 0, s>>>(nmax_dev, N, offsets_dev, blk);
-  offsets_fix_kernel<<<(unsigned)nblk, kThreads, 0, s>>>(N, nblk, offsets_dev, blk);
-  g_launches.fetch_add(2, std::memory_order_relaxed);
-  e = cudaGetLastError();
-  cudaFreeAsync(blk, s);
-  return cuda_status(e);
+  const int64_t nblk = (N + kScanTile - 1) / kScanTile;
+  if (nblk > INT32_MAX) return BOYS_E_ARG;
+  const bool vec = (reinterpret_cast<uintptr_t>(nmax_dev) & 15) == 0;
+  offsets_totals_kernel<<<(unsigned)nblk, kThreads, 0, s>>>(nmax_dev, N, offsets_dev, vec);
+  offsets_blocks_kernel<<<1, 1024, 0, s>>>(N, nblk, offsets_dev);
+  offsets_tiles_kernel<<<(unsigned)nblk, kThreads, 0, s>>>(nmax_dev, N, offsets_dev, vec);
+  g_launches.fetch_add(3, std::memory_order_relaxed);
+  return cuda_status(cudaGetLastError());
 }
 
 }  // namespace boys

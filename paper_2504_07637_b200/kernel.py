@@ -89,9 +89,73 @@ def _as_device_x(x) -> torch.Tensor:
     return x.contiguous().reshape(-1)
 
 
-def _boys_device(n_max: int, x: torch.Tensor, layout: str, out, expx: bool, check: bool):
+# ----------------------------------------------------------------------------
+# coefficient tables at the boundary
+# ----------------------------------------------------------------------------
+
+_PROFILE = {torch.float64: "double53", torch.float32: "single24"}
+_handles = {}          # (sha256, device index) -> boys_table* (kept for the process)
+
+
+def _kernel_table(table, dtype):
+    """table (coeffs.Dataset / coeffs.KernelTable / dataset path) -> KernelTable
+    of dtype's profile; ValueError for another profile or a malformed table."""
+    from . import coeffs as CF
+    if isinstance(table, (str, bytes)) or hasattr(table, "__fspath__"):
+        table = CF.load(table)
+    if isinstance(table, CF.Dataset):
+        table = CF.build_kernel_table(table)
+    if not isinstance(table, CF.KernelTable):
+        raise TypeError(f"table must be a coeffs.Dataset, coeffs.KernelTable or a dataset path, "
+                        f"got {type(table).__name__}")
+    want = _PROFILE[dtype]
+    if table.profile != want:
+        raise ValueError(f"table profile {table.profile!r} does not match {dtype} "
+                         f"(needs {want!r})")
+    return table
+
+
+def table_checksum(dtype=torch.float64) -> str:
+    """SHA-256 of the compiled-in table (coeffs.table_checksum of the shipped dataset)."""
+    dt = _DTYPES[_torch_dtype(dtype)]
+    return L.load().boys_table_checksum(dt).decode()
+
+
+def _table_handle(table, dtype, device):
+    """None -> the compiled tables; a table equal to them (same checksum) ->
+    None as well; any other table -> a device copy (uploaded once per device)."""
+    if table is None:
+        return None
+    from . import coeffs as CF
+    kt = _kernel_table(table, dtype)
+    digest = CF.table_checksum(kt)
+    if digest == table_checksum(dtype):
+        return None
+    key = (digest, torch.device(device).index)
+    h = _handles.get(key)
+    if h is None:
+        rows = CF.pack_rows(kt)
+        lib = L.load()
+        nb = lib.boys_table_row_bytes(_DTYPES[dtype])
+        if nb * len(kt.rows) != len(rows):
+            raise ValueError("table row layout does not match libboys")
+        buf = C.create_string_buffer(rows, len(rows))
+        hp = C.c_void_p()
+        with torch.cuda.device(device):
+            L.check(lib.boys_table_create(_DTYPES[dtype], C.cast(buf, C.c_void_p), len(kt.rows),
+                                          nb, C.byref(hp)))
+        h = _handles[key] = hp
+    return h
+
+
+def _boys_device(n_max: int, x: torch.Tensor, layout: str, out, expx: bool, check: bool,
+                 table=None):
     lay = _layout(layout)
     _check_order(n_max, x.dtype)
+    th = _table_handle(table, x.dtype, x.device)
+    if th is not None and n_max > L.load().boys_table_max_order(th):
+        raise ValueError(f"order {n_max} exceeds the table's maximum "
+                         f"{L.load().boys_table_max_order(th)}")
     xf = _as_device_x(x)
     N = xf.numel()
     shape = (n_max + 1, N) if lay == L.BOYS_SOA else (N, n_max + 1)
@@ -103,8 +167,14 @@ def _boys_device(n_max: int, x: torch.Tensor, layout: str, out, expx: bool, chec
     ex = torch.empty(N, dtype=x.dtype, device=x.device) if expx else None
     dom = torch.full((1,), -1, dtype=torch.int64, device=x.device) if check else None
     with torch.cuda.device(x.device):
-        L.check(L.load().boys_eval_dense(_DTYPES[x.dtype], n_max, _ptr(xf), N, _ptr(out), lay,
-                                         _ptr(ex), _ptr(dom), C.c_void_p(_stream_ptr(x.device))))
+        if th is None:
+            L.check(L.load().boys_eval_dense(_DTYPES[x.dtype], n_max, _ptr(xf), N, _ptr(out),
+                                             lay, _ptr(ex), _ptr(dom),
+                                             C.c_void_p(_stream_ptr(x.device))))
+        else:
+            L.check(L.load().boys_eval_dense_table(th, n_max, _ptr(xf), N, _ptr(out), lay,
+                                                   _ptr(ex), _ptr(dom),
+                                                   C.c_void_p(_stream_ptr(x.device))))
     if check:
         first = int(dom.item())
         if first >= 0:
@@ -145,16 +215,41 @@ def _boys_host(n_max: int, x, layout: str, out):
     return torch.from_numpy(res) if was_tensor else res
 
 
-def boys(n_max: int, x, *, layout: str = "soa", out=None, check: bool = True):
+def _to_device(x):
+    """Host input (numpy / list / scalar / CPU tensor) -> CUDA tensor, keeping
+    float32 and float64 (anything else becomes float64)."""
+    if isinstance(x, torch.Tensor):
+        t = x.detach()
+        if t.dtype not in _DTYPES:
+            t = t.to(torch.float64)
+        return t.cuda()
+    a = np.asarray(x)
+    if a.dtype not in (np.float64, np.float32):
+        a = a.astype(np.float64)
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def boys(n_max: int, x, *, layout: str = "soa", out=None, check: bool = True, table=None):
     """F_0..F_{n_max}(x) for every element of x (the batched boys_downward).
 
     x: CUDA tensor (float64 or float32) -> CUDA tensor, computed on the current
     stream; numpy array / list / CPU tensor -> host result via the pipelined
     host-buffer path.  Shape [n_max+1, N] ('soa') or [N, n_max+1] ('aos').
-    ``check=False`` skips the batch domain check (no host sync).
+    ``check=False`` skips the batch domain check (no host sync).  ``table``:
+    a coeffs.Dataset / KernelTable / dataset path; None or the compiled table
+    -> the compiled kernels, any other -> the uploaded-table path.
     """
     if isinstance(x, torch.Tensor) and x.is_cuda:
-        return _boys_device(n_max, x, layout, out, False, check)[0]
+        return _boys_device(n_max, x, layout, out, False, check, table)[0]
+    if table is not None:
+        dt = _torch_dtype(np.asarray(x).dtype if not isinstance(x, torch.Tensor) else x.dtype)
+        if _table_handle(table, dt or torch.float64, torch.device("cuda")) is not None:
+            xd = _to_device(x)
+            res = _boys_device(n_max, xd, layout, None, False, check, table)[0].cpu()
+            if out is not None:
+                (out if isinstance(out, torch.Tensor) else torch.from_numpy(out)).copy_(res)
+                return out
+            return res if isinstance(x, torch.Tensor) else res.numpy()
     return _boys_host(n_max, x, layout, out)
 
 
@@ -176,38 +271,49 @@ class EvalResult:
 
 
 def eval_batch(req: EvalRequest, table=None) -> EvalResult:
-    """SPEC.md:316-324.  ``table`` is accepted for signature parity; the
-    kernel tables are compiled into libboys (see coeffs.gen_header)."""
+    """SPEC.md:316-324.  ``table`` (coeffs.Dataset / KernelTable / dataset
+    path): None or the compiled table -> the compiled kernels; a different
+    table is uploaded once and evaluated by the run-time-table kernel."""
     x = req.xs
     if not (isinstance(x, torch.Tensor) and x.is_cuda):
-        x = torch.as_tensor(np.asarray(x)).cuda()
-        vals, ex = _boys_device(req.n, x, req.layout, None, True, True)
+        x = _to_device(x)
+        vals, ex = _boys_device(req.n, x, req.layout, None, True, True, table)
         return EvalResult(values=vals.cpu().numpy(), expx=ex.cpu().numpy())
-    vals, ex = _boys_device(req.n, x, req.layout, None, True, True)
+    vals, ex = _boys_device(req.n, x, req.layout, None, True, True, table)
     return EvalResult(values=vals, expx=ex)
 
 
 def eval_fn(n: int, x, table=None):
-    """(F_n(x), e^{-x}) for a batch (or a scalar) x."""
+    """(F_n(x), e^{-x}) for a batch (or a scalar) x, in x's
+    dtype (float32 stays float32)."""
     scalar = np.isscalar(x) or (isinstance(x, torch.Tensor) and x.dim() == 0)
-    xt = x if isinstance(x, torch.Tensor) and x.is_cuda else torch.as_tensor(
-        np.atleast_1d(np.asarray(x, dtype=np.float64))).cuda()
-    vals, ex = _boys_device(n, xt.reshape(-1), "soa", None, True, True)
+    if isinstance(x, torch.Tensor) and x.is_cuda:
+        xt = x
+    elif isinstance(x, torch.Tensor):
+        xt = _to_device(x.reshape(-1))
+    else:
+        xt = _to_device(np.atleast_1d(np.asarray(x)))
+    vals, ex = _boys_device(n, xt.reshape(-1), "soa", None, True, True, table)
     fn = vals[n]
     if scalar:
         return float(fn[0]), float(ex[0])
     return fn, ex
 
 
-def eval_with_split(n: int, n_bar: int, x, layout: str = "soa", check: bool = True, out=None):
+def eval_with_split(n: int, n_bar: int, x, table=None, layout: str = "soa", check: bool = True,
+                    out=None):
     """F_{n_bar+1..n} from the order-n seed, F_{0..n_bar} from
-    the order-n_bar seed (two recursions).  ``out``: optional preallocated
-    device tensor of the result's shape (device inputs only)."""
-    xt = x if isinstance(x, torch.Tensor) and x.is_cuda else torch.as_tensor(
-        np.asarray(x)).cuda()
+    the order-n_bar seed (two recursions).  ``table`` as in eval_batch.
+    ``out``: optional preallocated device tensor of the result's shape
+    (device inputs only)."""
+    xt = x if isinstance(x, torch.Tensor) and x.is_cuda else _to_device(x)
     _check_order(n, xt.dtype)
     if not isinstance(n_bar, (int, np.integer)) or not 0 <= n_bar < n:
         raise ValueError(f"need 0 <= n_bar < n, got n_bar={n_bar!r}, n={n}")
+    th = _table_handle(table, xt.dtype, xt.device)
+    if th is not None and n > L.load().boys_table_max_order(th):
+        raise ValueError(f"order {n} exceeds the table's maximum "
+                         f"{L.load().boys_table_max_order(th)}")
     lay = _layout(layout)
     xf = _as_device_x(xt)
     N = xf.numel()
@@ -219,8 +325,12 @@ def eval_with_split(n: int, n_bar: int, x, layout: str = "soa", check: bool = Tr
         raise ValueError(f"out must be a contiguous {xt.dtype} tensor of shape {shape}")
     dom = torch.full((1,), -1, dtype=torch.int64, device=xt.device) if check else None
     with torch.cuda.device(xt.device):
-        L.check(L.load().boys_eval_split(_DTYPES[xt.dtype], n, n_bar, _ptr(xf), N, _ptr(out), lay,
-                                         _ptr(dom), C.c_void_p(_stream_ptr(xt.device))))
+        if th is None:
+            L.check(L.load().boys_eval_split(_DTYPES[xt.dtype], n, n_bar, _ptr(xf), N, _ptr(out),
+                                             lay, _ptr(dom), C.c_void_p(_stream_ptr(xt.device))))
+        else:
+            L.check(L.load().boys_eval_split_table(th, n, n_bar, _ptr(xf), N, _ptr(out), lay,
+                                                   _ptr(dom), C.c_void_p(_stream_ptr(xt.device))))
     if check and int(dom.item()) >= 0:
         _domain_error(xf, int(dom.item()))
     return out if isinstance(x, torch.Tensor) and x.is_cuda else out.cpu().numpy()
@@ -286,14 +396,21 @@ def _boys_ragged_host(x, n_max, out, return_offsets: bool):
 
 
 def boys_ragged(x: torch.Tensor, n_max: torch.Tensor, offsets: torch.Tensor = None, *,
-                out: torch.Tensor = None, check: bool = True, return_offsets: bool = True):
+                out: torch.Tensor = None, check: bool = True, return_offsets: bool = True,
+                table=None):
     """Per-element orders: element i gets F_0..F_{n_max[i]}(x_i) at
     values[offsets[i] : offsets[i+1]].  Returns (values, offsets).
 
     x on a CUDA device: computed on the current stream (offsets as given, or
     the exclusive prefix sum of n_max + 1).  x (and n_max) on the host: the
     pipelined host-buffer path; results come back on the host, offsets are the
-    exclusive prefix sum (None with return_offsets=False)."""
+    exclusive prefix sum (None with return_offsets=False).  ``table``: ragged
+    batches run the compiled tables only; a different table raises ValueError."""
+    if table is not None:
+        dt = x.dtype if isinstance(x, torch.Tensor) else _torch_dtype(np.asarray(x).dtype)
+        if _table_handle(table, dt or torch.float64, torch.device("cuda")) is not None:
+            raise ValueError("ragged batches evaluate the compiled table only; use eval_batch "
+                             "per order for a different table")
     if not (isinstance(x, torch.Tensor) and x.is_cuda):
         return _boys_ragged_host(x, n_max, out, return_offsets)
     xf = _as_device_x(x)
@@ -302,6 +419,8 @@ def boys_ragged(x: torch.Tensor, n_max: torch.Tensor, offsets: torch.Tensor = No
         raise ValueError("n_max must be a uint8 tensor on x's device with one entry per x")
     if offsets is None:
         offsets = ragged_offsets(nm)
+    else:
+        offsets = offsets.contiguous().reshape(-1)
     if offsets.dtype != torch.int64 or offsets.numel() != xf.numel() + 1 or \
             offsets.device != xf.device:
         raise ValueError("offsets must be an int64 tensor of N+1 entries on x's device")

@@ -109,3 +109,15 @@ def test_c_example_compiles_and_links(tmp_path):
                     f"-Wl,-rpath,{B.PKG}", "-o", str(exe)], check=True)
     r = subprocess.run([str(exe)], capture_output=True, text=True)
     assert r.returncode == 64 and "usage" in r.stderr
+
+
+def test_compiled_table_checksum_without_gpu():
+    """libboys reports the digest of the table it was compiled with; it equals
+    coeffs.table_checksum of the shipped datasets (the boundary compares a
+    caller's table against it)."""
+    from paper_2504_07637_b200 import _lib, coeffs as C
+    L = _lib.load()
+    for dt, prof in ((_lib.BOYS_F64, "double53"), (_lib.BOYS_F32, "single24")):
+        kt = C.build_kernel_table(C.load_default(prof))
+        assert L.boys_table_checksum(dt).decode() == C.table_checksum(kt)
+        assert L.boys_table_row_bytes(dt) * len(kt.rows) == len(C.pack_rows(kt))
