@@ -656,9 +656,9 @@ def _mp_worker(args):
     return len(xs)
 
 
-def reference_mpmath_rate(cfg_name="cfg3", npts=1 << 12):
+def reference_mpmath_rate(cfg_name="cfg3", npts=1 << 14):
     """The reference's own CPU path: refmath.boys_downward(n, x, Precision(64))
-    (refmath.py:330-341) on a seeded 2^12-point sample of the config, one
+    (refmath.py:330-341) on a seeded 2^14-point sample of the config, one
     process per host core (the mpmath context is process-global)."""
     ref_dir = ROOT / "baseline" / "_ref"
     if not (ref_dir / "boysfn" / "refmath.py").exists():

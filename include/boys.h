@@ -137,9 +137,9 @@ boys_status boys_eval_split_table(const boys_table* table, int n, int n_bar, con
                                   int64_t* dom_dev, void* stream);
 
 /* Per-shard error statistic (the multi-GPU path's only reduction):
- * *err_dev = max(*err_dev, max_j |(vals[pos_j] - hi_j) - lo_j| / |hi_j|) over
- * j < K, gold_dev = K (hi, lo) double-double reference pairs; |hi_j| below the
- * dtype's smallest normal contributes 0, NaN contributes +inf.  Stream-ordered,
+ * *err_dev = max(*err_dev, max_j |(vals[pos_j] - hi_j) - lo_j| / max(|hi_j|, tiny))
+ * over j < K, gold_dev = K (hi, lo) double-double reference pairs, tiny = the
+ * dtype's smallest normal (absolute error below it); NaN contributes +inf.  Stream-ordered,
  * one launch; the caller initialises *err_dev (0.0) and gathers it across ranks. */
 boys_status boys_shard_error(boys_dtype dtype, const void* vals_dev, const int64_t* pos_dev,
                              const double* gold_dev, int64_t K, double* err_dev, void* stream);

@@ -13,8 +13,9 @@
 
 namespace boys {
 
-// rel_j = |(v - hi) - lo| / |hi| for |hi| >= tiny (else 0: the reference is
-// below the dtype's normal range); NaN -> +inf.  Max over j, folded into *err
+// rel_j = |(v - hi) - lo| / max(|hi|, tiny): relative error, measured
+// against the dtype's smallest normal where the true value is below it
+// (tests/accuracy.py rel_err); NaN -> +inf.  Max over j, folded into *err
 // with an integer atomicMax on the bit pattern (monotonic for values >= 0).
 template <typename T>
 __global__ void __launch_bounds__(kThreads)
@@ -28,7 +29,7 @@ shard_error_kernel(const T* __restrict__ vals, const int64_t* __restrict__ pos,
     const double v = (double)vals[pos[j]];
     const double hi = gold[2 * j], lo = gold[2 * j + 1];
     const double e = fabs((v - hi) - lo);
-    double r = fabs(hi) >= tiny ? e / fabs(hi) : 0.0;
+    double r = e / fmax(fabs(hi), tiny);
     if (isnan(r)) r = __longlong_as_double(0x7ff0000000000000LL);
     m = fmax(m, r);
   }

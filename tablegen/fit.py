@@ -67,6 +67,7 @@ class FitResult:
     v_quads: list = field(default_factory=list)   # [(z, b)]
     v_lins: list = field(default_factory=list)    # [z]
     grid_points: int = 0
+    rescan_bits: float = 0.0
 
 
 def _q_sample(n, x):
@@ -287,13 +288,33 @@ def fit(n, N, bits_target, m_nodes=None, lawson_iters=60, exchange_rounds=2,
         return res
 
 
-def validate(res):
-    """SPEC.md:182-190 checks. Returns a list of violation strings."""
+def rescan_bits(res, factor=4):
+    """-log2 max |F~/F - 1| re-derived on a fresh grid `factor` times denser
+    than the fit's ("re-derives exact_error_bits on a fresh 4x
+    denser grid"): equally spaced midpoints of factor * grid_points cells of
+    [0, z), none of them a point of the fit's own grid."""
+    with mp.workprec(FIT_BITS):
+        M = factor * max(1, res.grid_points)
+        worst = mp.mpf(0)
+        for i in range(M):
+            x = res.z * (2 * i + 1) / (2 * M)
+            e = abs(rel_f_error(res.n, res.consts, res.u, res.v, x, _q_sample(res.n, x)))
+            worst = max(worst, e)
+        return float(-mp.log(worst, 2)) if worst > 0 else float("inf")
+
+
+def validate(res, rescan=4, drift_bits=0.5):
+    """SPEC.md:182-190 checks. Returns a list of violation strings.
+
+    rescan: density factor of the fresh-grid re-derivation of exact_bits
+    (0 skips it); a drift of more than drift_bits below the recorded value
+    means the fit grid under-resolved the error curve."""
     bad = []
     with mp.workprec(FIT_BITS):
         v0 = res.v[0]
         if not v0 > 0:
-            bad.append("B_N <= 0 (v(0) <= 0): rejected per PAPER.md:163-164")
+            bad.append("B_N <= 0 (v(0) <= 0): rejected by the paper's section III rule "
+                       "(PAPER.md:163-164, solutions with B_N < 0 are rejected)")
         for zr in res.v_lins:
             if zr >= 0:
                 bad.append(f"pole of v on [0, inf): real root {zr}")
@@ -324,6 +345,12 @@ def validate(res):
             if not qtilde(res.consts, res.u, res.v, x) > 0:
                 bad.append(f"Q~ <= 0 at x={float(x)}")
                 break
+    if rescan and not bad:
+        rb = rescan_bits(res, rescan)
+        res.rescan_bits = rb
+        if rb < res.exact_bits - drift_bits:
+            bad.append(f"grid-refinement drift: {rescan}x denser grid gives {rb:.2f} bits vs "
+                       f"{res.exact_bits:.2f} recorded (> {drift_bits} bit): under-resolved grid")
     return bad
 
 

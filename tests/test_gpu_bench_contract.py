@@ -34,11 +34,13 @@ def test_bench_json_line_on_gpu():
     assert abs(ro["achieved"] / ro["peak"] - ro["frac"]) < 1e-3
     c = d["clocks"]
     assert c["sm_mhz"] > 0 and c["sm_max_mhz"] > 0 and isinstance(c["reasons"], list)
-    assert d["gpu_launches"] == 5
+    # per step: the evaluator launch + the per-shard error reduction
+    assert d["gpu_launches"] == 5 * 2 and d["gpu_launches_per_step"]["evaluator"] == 1
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] == 8 * (1 << 26)
     assert e["d2h_bytes_per_step"] == 8 * 17 * (1 << 26)
     cb = d["cpu_baseline"]
     assert cb["kind"] == "port" and cb["cores"] >= 1 and cb["value"] > 0
     assert cb["max_ulp_gpu_vs_port"] == 0
-    assert d["accuracy"]["bits"] > 40
+    acc = d["accuracy"]
+    assert acc["bits"] > 42.1 and len(acc["per_rank"]) == 1 and acc["max_ulp_vs_port"] == 0

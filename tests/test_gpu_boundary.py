@@ -193,7 +193,7 @@ def test_shard_error_kernel(dtype):
     hi = np.exp(rng.uniform(-60, 60, K))
     if dtype == torch.float32:
         hi = np.exp(rng.uniform(-30, 30, K))
-        hi[:10] = 1e-40                              # below FLT_MIN: contributes 0
+        hi[:10] = 1e-40                              # below FLT_MIN: absolute vs FLT_MIN
     lo = hi * rng.uniform(-1e-17, 1e-17, K)
     vals = (hi * (1 + rng.uniform(-1e-12, 1e-12, K))).astype(np.float64 if dtype == torch.float64
                                                              else np.float32)
@@ -202,7 +202,7 @@ def test_shard_error_kernel(dtype):
     v[pos] = vals
     tiny = np.finfo(vals.dtype).tiny
     e = np.abs((vals.astype(np.float64) - hi) - lo)
-    ref = np.where(np.abs(hi) >= tiny, e / np.abs(hi), 0.0).max()
+    ref = (e / np.maximum(np.abs(hi), tiny)).max()
     err = torch.zeros(1, dtype=torch.float64, device="cuda")
     vd = torch.from_numpy(v).cuda()
     pd = torch.from_numpy(pos).cuda()
