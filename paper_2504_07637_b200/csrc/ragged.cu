@@ -182,26 +182,31 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
     load(c + wstride);
     constexpr int MAXN = Tab<T>::MAX_ORDER;
     bool xok[EPL], slow = cnt > WarpT::CAP;
+    int cnt_l = 0;
 #pragma unroll
     for (int e = 0; e < EPL; ++e) {
       xok[e] = valid_x(x[e]);
       if (in[e] && !(xok[e] && n[e] <= MAXN)) flag_domain(dom, i0 + 32 * e + lane);
       slow = slow || (in[e] && n[e] > NB);
+      cnt_l += in[e] ? n[e] + 1 : 0;
     }
+    // offsets that are not the chunk's prefix sum (gaps between elements):
+    // the staged range would not match, so write per element at offsets[i]
+    const int64_t cnt_sum = (int64_t)__reduce_add_sync(kFull, (unsigned)cnt_l);   // every lane
+    slow = slow || cnt_sum != cnt;
     if (__any_sync(kFull, slow)) {
       // an order above the fast path's bound (or an output range above the
       // staging capacity): every lane evaluates its own elements from the
       // __constant__ rows and writes them directly (NaN above the table)
 #pragma unroll
       for (int e = 0; e < EPL; ++e) {
-        if (in[e] && n[e] > MAXN) {
+        const bool okl = in[e] && xok[e] && n[e] <= MAXN;
+        if (in[e] && !okl) {                       // NaN row (domain flagged above)
           for (int m = 0; m <= n[e]; ++m) out[goff[e] + m] = A::nan();
         }
-        const bool okl = in[e] && xok[e] && n[e] <= MAXN;
         T* dst = out + goff[e];
-        const bool wd = in[e] && n[e] <= MAXN;
         eval_point_rt<T, MAXN>(x[e], okl, okl ? n[e] : 0, ConstRows<T>{}, [&](int m, T v) {
-          if (wd) dst[m] = v;
+          if (okl) dst[m] = v;
         });
       }
       continue;

@@ -217,6 +217,44 @@ def test_ragged_cfg4_inputs(oracle):
     assert_parity(got.cpu().numpy(), ref, "cfg4 f32")
 
 
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_ragged_window_paths(oracle, dtype):
+    """The sorted-window kernel's other paths, bit-exact against the oracle:
+    offsets that are not the prefix sum (gaps between elements: per-element
+    writes through offsets[i], gap slots untouched), inputs that are not
+    16-byte aligned (no bulk loads), invalid x inside full windows (NaN rows),
+    and high orders mixed into ERI-like windows."""
+    rng = np.random.default_rng(21)
+    N = 3 * 1024 + 517
+    mx = max_order(dtype)
+    x = dense_inputs(dtype, 12, N=N)[:N]
+    nm = rng.integers(0, 13, size=N).astype(np.uint8)
+    ref, roff, bad = oracle.ragged(x, nm)
+    # gapped offsets: element i starts 3*i slots later than the prefix sum
+    off_g = roff + 3 * np.arange(N + 1, dtype=np.int64)
+    tg = torch.from_numpy(off_g).cuda()
+    outg = torch.full((int(off_g[-1]),), -7.0, dtype=torch.from_numpy(x).dtype, device="cuda")
+    boys_ragged(torch.from_numpy(x).cuda(), torch.from_numpy(nm).cuda(), tg, out=outg)
+    g = outg.cpu().numpy()
+    for i in range(N):
+        assert np.array_equal(g[off_g[i]:off_g[i] + nm[i] + 1].view(np.uint8),
+                              ref[roff[i]:roff[i + 1]].view(np.uint8))
+        assert np.all(g[off_g[i] + nm[i] + 1:off_g[i + 1]] == -7.0)
+    # misaligned x / n_max views (element-aligned only)
+    xb = torch.from_numpy(np.concatenate([x[:1], x])).cuda()
+    nb = torch.from_numpy(np.concatenate([nm[:1], nm])).cuda()
+    got, _ = boys_ragged(xb[1:], nb[1:])
+    assert_parity(got.cpu().numpy(), ref, "ragged misaligned inputs")
+    # invalid x and high orders inside full windows
+    x2, n2 = x.copy(), nm.copy()
+    x2[[5, 1500, 2047]] = np.nan
+    x2[[7, 3000]] = -1.0
+    n2[2100:2110] = mx
+    ref2, roff2, bad2 = oracle.ragged(x2, n2)
+    got2, _ = boys_ragged(torch.from_numpy(x2).cuda(), torch.from_numpy(n2).cuda(), check=False)
+    assert_parity(got2.cpu().numpy(), ref2, "ragged invalid / high orders")
+
+
 def test_ragged_domain_and_order_errors():
     x = torch.tensor([1.0, 2.0, -3.0], device="cuda", dtype=torch.float64)
     nm = torch.tensor([1, 2, 3], device="cuda", dtype=torch.uint8)
