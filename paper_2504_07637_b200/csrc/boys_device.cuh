@@ -22,9 +22,6 @@ constexpr unsigned kFull = 0xffffffffu;
 #ifndef BOYS_PAIR_MINB_SMALL
 #define BOYS_PAIR_MINB_SMALL 5   // paired SoA kernel, n <= 1: resident-block target (47 registers; cfg1 9.27 us vs 9.50 / 9.71 / 9.65 / 9.75 for 6 / 4 / 3 / 8)
 #endif
-#ifndef BOYS_PAIR_FASTCR
-#define BOYS_PAIR_FASTCR 0   // 1: paired SoA kernel shares fast-path checks for div/sqrt/rcp (A/B: slower, spills: cfg1 10.7 vs 9.5 us)
-#endif
 #ifndef BOYS_FAST_CR
 #define BOYS_FAST_CR 0   // 1: ragged chunks use the branch-free CR rcp/sqrt fast paths (A/B: f64 1.88 vs 1.83 ms, slower)
 #endif
@@ -111,7 +108,8 @@ __device__ __forceinline__ T eval_point_stream(T x_in, bool ok, Put&& put) {
     put(m, cur);
   }
   bool up = ok && x > R.x_up;
-  if (__any_sync(kFull, up)) {
+  // n = 0: the ladder's F_0 = c_0 sqrt(1/x) is the y = x seed itself
+  if (n > 0 && __any_sync(kFull, up)) {
     T rx = A::rcp(x);
     T f = up_first(x);
     if (up) put(0, f);
@@ -130,55 +128,86 @@ __device__ __forceinline__ void eval_point(T x_in, bool ok, T (&Fv)[n + 1], T& t
   t_out = eval_point_stream<T, n>(x_in, ok, [&](int m, T v) { Fv[m] = v; });
 }
 
-// seed<double, n> for two points with the correctly rounded div / sqrt / rcp
-// taken through their branch-free fast paths (boys_eval.cuh, bit-identical to
-// the intrinsics): one warp vote per operation decides whether any lane needs
-// the intrinsic instead, so the two chains share one check per operation.
-template <int n>
-__device__ __forceinline__ void seed_pair(const double (&x)[2], const double (&t)[2],
-                                          bool any_below, double (&F)[2]) {
+// seed<double, n> for P points with the correctly rounded div / sqrt / rcp
+// taken through their branch-free fast paths (boys_eval.cuh: ptxas's own fast
+// path and range test, bit-identical to the intrinsics): one warp vote per
+// operation decides whether any lane needs the intrinsic instead (then every
+// point of the thread recomputes that operation with it), so the P chains
+// interleave without a branch region per call.  The FP64-bound small orders'
+// multi-point SoA kernels use it.
+template <int n, int P>
+__device__ __forceinline__ void seed_multi_fast(const double (&x)[P], const double (&t)[P],
+                                                bool any_below, double (&F)[P]) {
   using A = Ar<double>;
   const BoysRow<double>& R = Tab<double>::row(n);
-  double y[2] = {x[0], x[1]};
+  constexpr int LU = Tab<double>::shape(n, 0), lu = Tab<double>::shape(n, 1);
+  constexpr int LV = Tab<double>::shape(n, 2), lv = Tab<double>::shape(n, 3);
+  double y[P];
+#pragma unroll
+  for (int j = 0; j < P; ++j) y[j] = x[j];
   if (any_below) {
-    constexpr int LU = Tab<double>::shape(n, 0), lu = Tab<double>::shape(n, 1);
-    constexpr int LV = Tab<double>::shape(n, 2), lv = Tab<double>::shape(n, 3);
-    double u[2], v[2], w[2], Q[2], sq[2];
+    double w[P], Q[P], sq[P];
+    bool slow = false;
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      u[j] = factored<double, LU, lu>(x[j], R.uq, R.ul);
-      v[j] = factored<double, LV, lv>(x[j], R.vq, R.vl);
+    for (int j = 0; j < P; ++j) {
+      const double u = factored<double, LU, lu>(x[j], R.uq, R.ul);
+      const double v = factored<double, LV, lv>(x[j], R.vq, R.vl);
+      bool sj;
+      w[j] = A::div_fast(u, v, sj);
+      slow = slow || sj;
     }
-    bool s0, s1;
-    w[0] = A::div_fast(u[0], v[0], s0);
-    w[1] = A::div_fast(u[1], v[1], s1);
-    if (__any_sync(kFull, s0 || s1)) { w[0] = A::div(u[0], v[0]); w[1] = A::div(u[1], v[1]); }
+    if (__any_sync(kFull, slow)) {               // (never for finite x >= 0 in practice)
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
+      for (int j = 0; j < P; ++j)
+        w[j] = A::div(factored<double, LU, lu>(x[j], R.uq, R.ul),
+                      factored<double, LV, lv>(x[j], R.vq, R.vl));
+    }
+    slow = false;
+#pragma unroll
+    for (int j = 0; j < P; ++j) {
       double h = A::mul(R.q2, w[j]);
       h = A::fma(h, x[j], R.q1);
       Q[j] = A::fma(h, x[j], R.q0);
+      bool sj;
+      sq[j] = A::sqrt_fast(Q[j], sj);
+      slow = slow || sj;
     }
-    sq[0] = A::sqrt_fast(Q[0], s0);
-    sq[1] = A::sqrt_fast(Q[1], s1);
-    if (__any_sync(kFull, s0 || s1)) { sq[0] = A::sqrt(Q[0]); sq[1] = A::sqrt(Q[1]); }
+    if (__any_sync(kFull, slow)) {
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
+      for (int j = 0; j < P; ++j) sq[j] = A::sqrt(Q[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < P; ++j) {
       const double s = n == 0 ? sq[j] : A::mul(powi<double, (n == 0 ? 1 : n)>(Q[j]), sq[j]);
       const double yq = A::fma(s, t[j], x[j]);
       y[j] = x[j] < R.z ? yq : x[j];
     }
   }
-  double r[2], sr[2];
-  bool s0, s1;
-  r[0] = A::rcp_fast(y[0], s0);
-  r[1] = A::rcp_fast(y[1], s1);
-  if (__any_sync(kFull, s0 || s1)) { r[0] = A::rcp(y[0]); r[1] = A::rcp(y[1]); }
-  sr[0] = A::sqrt_fast(r[0], s0);
-  sr[1] = A::sqrt_fast(r[1], s1);
-  if (__any_sync(kFull, s0 || s1)) { sr[0] = A::sqrt(r[0]); sr[1] = A::sqrt(r[1]); }
+  double r[P], sr[P];
+  bool slow = false;
 #pragma unroll
-  for (int j = 0; j < 2; ++j)
+  for (int j = 0; j < P; ++j) {
+    bool sj;
+    r[j] = A::rcp_fast(y[j], sj);
+    slow = slow || sj;
+  }
+  if (__any_sync(kFull, slow)) {
+#pragma unroll
+    for (int j = 0; j < P; ++j) r[j] = A::rcp(y[j]);
+  }
+  slow = false;
+#pragma unroll
+  for (int j = 0; j < P; ++j) {
+    bool sj;
+    sr[j] = A::sqrt_fast(r[j], sj);
+    slow = slow || sj;
+  }
+  if (__any_sync(kFull, slow)) {
+#pragma unroll
+    for (int j = 0; j < P; ++j) sr[j] = A::sqrt(r[j]);
+  }
+#pragma unroll
+  for (int j = 0; j < P; ++j)
     F[j] = n == 0 ? A::mul(R.c, sr[j])
                   : A::mul(A::mul(R.c, powi<double, (n == 0 ? 1 : n)>(r[j])), sr[j]);
 }
@@ -190,7 +219,7 @@ __device__ __forceinline__ void seed_pair(const double (&x)[2], const double (&t
 // P points per thread in lockstep (generalises eval_pair_stream; per point the
 // same operation sequence as eval_point_stream).  put(m, v[P]) gets F_m of all
 // P points; put1(j, m, v) the upward-ladder values of point j.
-template <typename T, int n, int P, typename Put, typename Put1>
+template <typename T, int n, int P, bool FAST = false, typename Put, typename Put1>
 __device__ __forceinline__ void eval_multi_stream(const T (&xin)[P], const bool (&ok)[P],
                                                   T (&tout)[P], Put&& put, Put1&& put1) {
   using A = Ar<T>;
@@ -205,8 +234,12 @@ __device__ __forceinline__ void eval_multi_stream(const T (&xin)[P], const bool 
     below = below || (ok[j] && x[j] < R.z);
   }
   const bool any_below = __any_sync(kFull, below);
+  if constexpr (FAST && sizeof(T) == 8) {
+    seed_multi_fast<n, P>(x, t, any_below, cur);
+  } else {
 #pragma unroll
-  for (int j = 0; j < P; ++j) cur[j] = seed<T, n>(x[j], t[j], any_below);
+    for (int j = 0; j < P; ++j) cur[j] = seed<T, n>(x[j], t[j], any_below);
+  }
   put(n, cur);
 #pragma unroll
   for (int j = 0; j < P; ++j) tx[j] = A::add(x[j], x[j]);
@@ -218,7 +251,8 @@ __device__ __forceinline__ void eval_multi_stream(const T (&xin)[P], const bool 
   }
 #pragma unroll
   for (int j = 0; j < P; ++j) up = up || (ok[j] && x[j] > R.x_up);
-  if (__any_sync(kFull, up)) {
+  // n = 0: the ladder's F_0 = c_0 sqrt(1/x) is the y = x seed itself
+  if (n > 0 && __any_sync(kFull, up)) {
 #pragma unroll
     for (int j = 0; j < P; ++j) {
       const bool upj = ok[j] && x[j] > R.x_up;
@@ -252,10 +286,6 @@ __device__ __forceinline__ void eval_pair_stream(T xa, T xb, bool oka, bool okb,
     below = below || (ok[j] && x[j] < R.z);
   }
   const bool any_below = __any_sync(kFull, below);
-#if BOYS_PAIR_FASTCR
-  if constexpr (sizeof(T) == 8) seed_pair<n>(x, t, any_below, cur);
-  else
-#endif
   {
 #pragma unroll
     for (int j = 0; j < 2; ++j) cur[j] = seed<T, n>(x[j], t[j], any_below);
@@ -271,7 +301,8 @@ __device__ __forceinline__ void eval_pair_stream(T xa, T xb, bool oka, bool okb,
   }
 #pragma unroll
   for (int j = 0; j < 2; ++j) up = up || (ok[j] && x[j] > R.x_up);
-  if (__any_sync(kFull, up)) {
+  // n = 0: the ladder's F_0 = c_0 sqrt(1/x) is the y = x seed itself
+  if (n > 0 && __any_sync(kFull, up)) {
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
       const bool upj = ok[j] && x[j] > R.x_up;

@@ -62,7 +62,7 @@ dense_soa_pair_kernel(const T* __restrict__ X, int64_t N, T* __restrict__ out,
 // two 16-byte loads, every F_m row as two 16-byte streaming stores.  N % 4 == 0
 // and 16-byte aligned buffers (host checks).  A/B variant for the FP64-bound
 // small orders.
-template <typename T, int n, int MINB>
+template <typename T, int n, int MINB, bool FAST>
 __global__ void __launch_bounds__(kThreads, MINB)
 dense_soa_quad_kernel(const T* __restrict__ X, int64_t N, T* __restrict__ out,
                       T* __restrict__ expx, int64_t* __restrict__ dom, int64_t index_base) {
@@ -83,15 +83,20 @@ dense_soa_quad_kernel(const T* __restrict__ X, int64_t N, T* __restrict__ out,
     } else {
       xv[0] = xv[1] = xv[2] = xv[3] = T(0);
     }
+    bool bad = false;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      ok[j] = valid_x(xv[j]);
-      if (in && !ok[j]) flag_domain(dom, index_base + i + j);
-      ok[j] = ok[j] || !in;
+      ok[j] = valid_x(xv[j]) || !in;
+      bad = bad || !ok[j];
+    }
+    if (__any_sync(kFull, bad)) {                  // rare: one vote per thread, not a branch per point
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (!ok[j]) flag_domain(dom, index_base + i + j);
     }
     T* o = out + i;
     T tv[4];
-    eval_multi_stream<T, n, 4>(
+    eval_multi_stream<T, n, 4, FAST>(
         xv, ok, tv,
         [&](int m, const T (&v)[4]) {
           if (in) {
@@ -405,7 +410,9 @@ static boys_status launch_soa_pair(const T* x, int64_t N, T* out, T* expx, int64
 template <typename T, int n>
 static boys_status launch_soa_quad(const T* x, int64_t N, T* out, T* expx, int64_t* dom,
                                    int64_t base, cudaStream_t s) {
-  auto k = dense_soa_quad_kernel<T, n, BOYS_QUAD_MINB>;
+  static const int fast = env_int("BOYS_QUAD_FASTCR", 1);
+  auto k = fast ? dense_soa_quad_kernel<T, n, BOYS_QUAD_MINB, true>
+                : dense_soa_quad_kernel<T, n, BOYS_QUAD_MINB, false>;
   const int64_t ntiles = (N + 4 * kThreads - 1) / (4 * kThreads);
   // one block per 1024-point tile (BOYS_GRID_TILES=2: persistent grid, slower: cfg1 10.8 vs 9.25 us)
   const int grid = (grid_tiles() != 2 && ntiles <= ((int64_t)1 << 30)) ? (int)ntiles
