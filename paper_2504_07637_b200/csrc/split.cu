@@ -17,8 +17,84 @@ namespace boys {
 // ---------------------------------------------------------------------------
 // split kernel (eval_with_split): F_m for m <= nbar equals a
 // dense order-nbar evaluation, F_m for m > nbar a dense order-n evaluation.
+// One e^{-x} per point serves both seeds; the order-n recursion stops at
+// nbar + 1 (its lower values are never used).  NBAR >= 0: compile-time lower
+// order (the common pairs); NBAR < 0: run-time nbar (uniform loops).
 // ---------------------------------------------------------------------------
-template <typename T, int n, bool AOS, int NBUF>
+template <typename T, int n, int NBAR, typename Put>
+__device__ __forceinline__ void split_point(T x_in, bool ok, int nbar_rt, Put&& put) {
+  using A = Ar<T>;
+  const int nbar = NBAR >= 0 ? NBAR : nbar_rt;      // warp-uniform
+  const T x = ok ? x_in : A::nan();                  // NaN through every step
+  const T t = exp_neg_clamped(x);
+  const T tx = A::add(x, x);
+  {
+    // order n: seed, recursion n-1 .. nbar+1
+    const BoysRow<T>& R = Tab<T>::row(n);
+    T cur = seed<T, n>(x, t, __any_sync(kFull, ok && x < R.z));
+    put(n, cur);
+#pragma unroll
+    for (int m = n - 1; m >= 0; --m) {
+      if (m <= nbar) break;
+      cur = A::mul(A::fma(tx, cur, t), rinv<T>(m));
+      put(m, cur);
+    }
+  }
+  if constexpr (NBAR >= 0) {
+    // order nbar (compile time): seed, recursion nbar-1 .. 0
+    const BoysRow<T>& R = Tab<T>::row(NBAR);
+    T cur = seed<T, NBAR>(x, t, __any_sync(kFull, ok && x < R.z));
+    put(NBAR, cur);
+#pragma unroll
+    for (int m = NBAR - 1; m >= 0; --m) {
+      cur = A::mul(A::fma(tx, cur, t), rinv<T>(m));
+      put(m, cur);
+    }
+  } else {
+    // order nbar (run time, uniform): the operation sequence of seed<T, nbar>
+    constexpr int MQ = MaxShape<T>::Q(), ML = MaxShape<T>::L();
+    const BoysRow<T>& R = Tab<T>::row(nbar);
+    const int bits = 32 - __clz(nbar | 1);
+    T y = x;
+    if (__any_sync(kFull, ok && x < R.z)) {
+      const T u = factored_uniform<T, MQ, ML>(x, R.uq, R.ul, R.cnt[0], R.cnt[1]);
+      const T v = factored_uniform<T, MQ, ML>(x, R.vq, R.vl, R.cnt[2], R.cnt[3]);
+      T h = A::mul(R.q2, A::div(u, v));
+      h = A::fma(h, x, R.q1);
+      const T Q = A::fma(h, x, R.q0);
+      const T sq = A::sqrt(Q);
+      const T s = nbar == 0 ? sq : A::mul(powi_rt_bounded(Q, nbar, bits), sq);
+      const T yq = A::fma(s, t, x);
+      y = x < R.z ? yq : x;
+    }
+    const T r = A::rcp(y);
+    const T sr = A::sqrt(r);
+    T cur = A::mul(A::mul(R.c, powi_rt_bounded(r, nbar, bits)), sr);   // nbar = 0: c * 1.0 == c
+    put(nbar, cur);
+#pragma unroll
+    for (int m = n - 2; m >= 0; --m) {
+      if (m < nbar) {
+        cur = A::mul(A::fma(tx, cur, t), rinv<T>(m));
+        put(m, cur);
+      }
+    }
+  }
+  // upward ladder past x_up (order-n values above nbar, order-nbar ones below)
+  const bool up_hi = ok && x > Tab<T>::row(n).x_up;
+  const bool up_lo = ok && x > Tab<T>::row(nbar).x_up;
+  if (__any_sync(kFull, up_hi || up_lo)) {
+    const T rx = A::rcp(x);
+    T f = up_first(x);
+    if (up_lo) put(0, f);
+#pragma unroll
+    for (int m = 0; m < n; ++m) {
+      f = up_next(f, m, rx);
+      if (m + 1 <= nbar ? up_lo : up_hi) put(m + 1, f);
+    }
+  }
+}
+
+template <typename T, int n, int NBAR, bool AOS, int NBUF>
 __global__ void __launch_bounds__(kThreads, AOS ? 4 : BOYS_SPLIT_SOA_MINB)
 split_kernel(const T* __restrict__ X, int64_t N, int nbar, T* __restrict__ out,
              int64_t* __restrict__ dom, bool bulk_ok) {
@@ -45,8 +121,7 @@ split_kernel(const T* __restrict__ X, int64_t N, int nbar, T* __restrict__ out,
       if (tid == 0) bulk_wait_read<NBUF - 1>();
       __syncthreads();
       T* row = buf + tid * W;
-      eval_point_stream<T, n>(x, ok, [&](int m, T v) { if (m > nbar) row[m] = v; });
-      eval_point_uniform<T, n>(x, ok, nbar, ConstRows<T>{}, [&](int m, T v) { if (m <= nbar) row[m] = v; });
+      split_point<T, n, NBAR>(x, ok, nbar, [&](int m, T v) { row[m] = v; });
       const int64_t cnt = (N - i0) < kThreads ? (N - i0) : kThreads;
       if (bulk_ok && cnt == kThreads) {
         fence_proxy_async_smem();
@@ -59,11 +134,8 @@ split_kernel(const T* __restrict__ X, int64_t N, int nbar, T* __restrict__ out,
       }
     } else {
       T* o = out + i;
-      eval_point_stream<T, n>(x, ok, [&](int m, T v) {
-        if (in && m > nbar) __stcs(o + (int64_t)m * N, v);
-      });
-      eval_point_uniform<T, n>(x, ok, nbar, ConstRows<T>{}, [&](int m, T v) {
-        if (in && m <= nbar) __stcs(o + (int64_t)m * N, v);
+      split_point<T, n, NBAR>(x, ok, nbar, [&](int m, T v) {
+        if (in) __stcs(o + (int64_t)m * N, v);
       });
     }
   }
@@ -75,11 +147,19 @@ static boys_status launch_split_t(const T* x, int64_t N, int nbar, T* out, int64
                                   cudaStream_t s) {
   constexpr bool fits2 = 2 * kThreads * (n + 1) * sizeof(T) <= 80 * 1024;
   constexpr int NBUF = (AOS && fits2) ? 2 : 1;
-  auto k = split_kernel<T, n, AOS, NBUF>;
+  // compile-time lower order for the common pairs: n_bar = n - 1 (one more
+  // order: "a few more bits") and n_bar = n / 2
+  // (orders above 16 only run-time nbar: compile time and library size)
+  constexpr bool SPEC = n <= 16;
+  constexpr int NB1 = SPEC ? n - 1 : -1, NB2 = SPEC ? n / 2 : -1;
+  const int var = (SPEC && nbar == NB1) ? 0 : (SPEC && nbar == NB2) ? 1 : 2;
+  auto k = var == 0   ? split_kernel<T, n, NB1, AOS, NBUF>
+           : var == 1 ? split_kernel<T, n, NB2, AOS, NBUF>
+                      : split_kernel<T, n, -1, AOS, NBUF>;
   const size_t smem = AOS ? (size_t)NBUF * kThreads * (n + 1) * sizeof(T) : 0;
-  static std::atomic<uint64_t> attr_mask{0};
+  static std::atomic<uint64_t> attr_mask[3];         // per kernel variant, per device
   if (AOS) {
-    boys_status st = opt_in_smem(k, (int)smem, attr_mask);
+    boys_status st = opt_in_smem(k, (int)smem, attr_mask[var]);
     if (st != BOYS_OK) return st;
   }
   const int64_t ntiles = (N + kThreads - 1) / kThreads;

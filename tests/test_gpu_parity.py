@@ -269,7 +269,9 @@ def test_ragged_domain_and_order_errors():
 def test_split_bit_exact(oracle, dtype):
     mx = max_order(dtype)
     x = dense_inputs(dtype, mx, N=3000)
-    for n, nbar in ((mx, mx - 1), (mx, 0), (mx, mx // 2), (3, 1), (1, 0)):
+    # compile-time lower orders (n <= 16: n_bar = n - 1 and n / 2) and run-time ones
+    for n, nbar in ((mx, mx - 1), (mx, 0), (mx, mx // 2), (3, 1), (1, 0), (16, 15), (16, 8),
+                    (16, 3), (12, 6), (12, 0), (9, 4), (2, 1)):
         for layout in ("soa", "aos"):
             got = eval_with_split(n, nbar, torch.from_numpy(x).cuda(), layout=layout)
             ref, bad = oracle.split(n, nbar, x, layout)
