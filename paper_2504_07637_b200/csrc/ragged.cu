@@ -358,18 +358,24 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
 // 1.00 ms) and was removed; it is in the history up to commit 50d605b.)
 
 // ---------------------------------------------------------------------------
-// ragged offsets: exclusive prefix sum of (n_i + 1), O(N) in three launches
-// and no workspace.  The output array itself holds the block totals:
-//   1. block b sums its tile and stores the total at OFF[min((b+1) TILE, N)]
-//      -- a slot that pass 3 (block b+1) or pass 2 (OFF[N]) overwrites;
-//   2. one block scans the nblk totals (strided reads) and writes block b's
-//      exclusive prefix to OFF[b TILE] and the grand total to OFF[N];
-//   3. block b scans its tile from that prefix (shared-memory transpose, so
-//      the int64 stores leave coalesced).
-// Traffic: n_max read twice + offsets written once.
+// ragged offsets: exclusive prefix sum of (n_i + 1), O(N), no workspace.  The
+// output array itself parks the nblk tile totals R and the ngrp group sums GS
+// contiguously at its tail (GS, R = OFF[N + 1 - ngrp - nblk .. N], inside the
+// last few tiles):
+//   1. block b sums its tiles' orders and stores R[b] (coalesced, 4 tiles per
+//      block, all loads in flight);
+//   2. block g scans R[1024 g ..] in place (exclusive, within the group) and
+//      parks the group's sum GS[g] just before R;
+//   3. block b < tfirst takes R[b] + sum(GS[< b/1024]) and scans its tile from
+//      it (shared-memory transpose, so the int64 stores leave coalesced);
+//      tiles tfirst.. overlap the parked words and are left to
+//   4. one block that first reads their prefixes, then writes those tiles and
+//      OFF[N] (the grand total).
+// Traffic: n_max read twice + offsets written once (~1.21 GB at 2^27).
 // ---------------------------------------------------------------------------
 constexpr int kScanPer = 16;                         // elements per thread
-constexpr int kScanTile = kThreads * kScanPer;       // 4096 elements per block
+constexpr int kScanTile = kThreads * kScanPer;       // 4096 elements per tile
+constexpr int kTotTiles = 4;                         // tiles per totals block
 
 // the thread's 16 consecutive orders (16-byte vector load when aligned)
 __device__ __forceinline__ void scan_load16(const uint8_t* __restrict__ NM, int64_t N, int64_t i0,
@@ -383,6 +389,21 @@ __device__ __forceinline__ void scan_load16(const uint8_t* __restrict__ NM, int6
 #pragma unroll
     for (int k = 0; k < kScanPer; ++k) v[k] = (i0 + k < N) ? (int)NM[i0 + k] + 1 : 0;
   }
+}
+
+// sum of (n + 1) over 16 consecutive orders (SIMD byte sums when aligned)
+__device__ __forceinline__ int scan_sum16(const uint8_t* __restrict__ NM, int64_t N, int64_t i0,
+                                          bool vec) {
+  if (vec && i0 + kScanPer <= N) {
+    const uint4 q = __ldg(reinterpret_cast<const uint4*>(NM + i0));
+    // __vsadu4(w, 0): sum of the 4 bytes of w
+    return (int)(__vsadu4(q.x, 0u) + __vsadu4(q.y, 0u) + __vsadu4(q.z, 0u) + __vsadu4(q.w, 0u)) +
+           kScanPer;
+  }
+  int s = 0;
+#pragma unroll
+  for (int k = 0; k < kScanPer; ++k) s += (i0 + k < N) ? (int)NM[i0 + k] + 1 : 0;
+  return s;
 }
 
 // block-wide exclusive scan of one int64 per thread (warp shuffles + 8 warp sums)
@@ -408,92 +429,141 @@ __device__ __forceinline__ int64_t block_excl_scan(int64_t v, int64_t* s_warp, i
 }
 
 __global__ void __launch_bounds__(kThreads)
-offsets_totals_kernel(const uint8_t* __restrict__ NM, int64_t N, int64_t* __restrict__ OFF,
-                      bool vec) {
-  __shared__ int64_t s_warp[kThreads / 32];
-  const int64_t b0 = (int64_t)blockIdx.x * kScanTile;
-  int v[kScanPer];
-  scan_load16(NM, N, b0 + (int64_t)threadIdx.x * kScanPer, vec, v);
-  int sum = 0;
-#pragma unroll
-  for (int k = 0; k < kScanPer; ++k) sum += v[k];
-  int64_t total;
-  block_excl_scan(sum, s_warp, total);
-  if (threadIdx.x == 0) OFF[min(b0 + kScanTile, N)] = total;
-}
-
-// one block: exclusive prefix of the block totals, in place
-__global__ void __launch_bounds__(1024)
-offsets_blocks_kernel(int64_t N, int64_t nblk, int64_t* __restrict__ OFF) {
-  __shared__ int64_t s_warp[32];
-  __shared__ int64_t s_carry;
+offsets_totals_kernel(const uint8_t* __restrict__ NM, int64_t N, int32_t* __restrict__ R,
+                      int64_t nblk, bool vec) {
+  __shared__ int s_warp[kTotTiles][kThreads / 32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  if (threadIdx.x == 0) s_carry = 0;
-  __syncthreads();
-  // rounds of 1024 * 8 totals: thread t takes 8 consecutive blocks
-  constexpr int PER = 8;
-  for (int64_t r0 = 0; r0 < nblk; r0 += 1024 * PER) {
-    const int64_t b0 = r0 + (int64_t)threadIdx.x * PER;
-    int64_t t[PER], sum = 0;
+  int sum[kTotTiles];
 #pragma unroll
-    for (int k = 0; k < PER; ++k) {
-      const int64_t b = b0 + k;
-      t[k] = b < nblk ? OFF[min((b + 1) * kScanTile, N)] : 0;
-      sum += t[k];
-    }
-    int64_t inc = sum;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const int64_t o = __shfl_up_sync(kFull, inc, d);
-      if (lane >= d) inc += o;
-    }
-    if (lane == 31) s_warp[wid] = inc;
-    __syncthreads();                       // every total of this round has been read
-    int64_t wpre = 0, total = 0;
-    for (int w = 0; w < 32; ++w) {
-      const int64_t s = s_warp[w];
-      wpre += w < wid ? s : 0;
-      total += s;
-    }
-    int64_t p = s_carry + wpre + inc - sum;
-#pragma unroll
-    for (int k = 0; k < PER; ++k) {
-      const int64_t b = b0 + k;
-      if (b < nblk) OFF[b * kScanTile] = p;     // b = 0 writes OFF[0] = 0
-      p += t[k];
-    }
-    __syncthreads();                       // s_warp / s_carry reuse
-    if (threadIdx.x == 0) s_carry += total;
-    __syncthreads();
+  for (int q = 0; q < kTotTiles; ++q) {       // loads of the block's tiles all in flight
+    const int64_t b = (int64_t)blockIdx.x * kTotTiles + q;
+    sum[q] = b < nblk ? scan_sum16(NM, N, b * kScanTile + (int64_t)threadIdx.x * kScanPer, vec) : 0;
   }
-  if (threadIdx.x == 0) OFF[N] = s_carry;
+#pragma unroll
+  for (int q = 0; q < kTotTiles; ++q) {
+    const int s = __reduce_add_sync(kFull, (unsigned)sum[q]);
+    if (lane == 0) s_warp[q][wid] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < kTotTiles) {
+    const int q = threadIdx.x;
+    const int64_t b = (int64_t)blockIdx.x * kTotTiles + q;
+    int t = 0;                               // <= 4096 * 256: int32
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w) t += s_warp[q][w];
+    if (b < nblk) R[b] = t;
+  }
 }
 
-__global__ void __launch_bounds__(kThreads)
-offsets_tiles_kernel(const uint8_t* __restrict__ NM, int64_t N, int64_t* __restrict__ OFF,
-                     bool vec) {
-  __shared__ int64_t s_warp[kThreads / 32];
+// group g (1024 totals, one per thread): R[g*1024 ..] <- exclusive prefix
+// sums within the group, in place; GS[g] <- the group's sum
+__global__ void __launch_bounds__(1024)
+offsets_groups_kernel(int64_t nblk, int32_t* __restrict__ R, int64_t* __restrict__ GS) {
+  __shared__ int64_t s_warp[32];
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const int64_t b = (int64_t)blockIdx.x * 1024 + t;
+  const int64_t v = b < nblk ? (int64_t)R[b] : 0;
+  int64_t inc = v;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int64_t o = __shfl_up_sync(kFull, inc, d);
+    if (lane >= d) inc += o;
+  }
+  if (lane == 31) s_warp[wid] = inc;
+  __syncthreads();
+  int64_t wpre = 0, total = 0;
+#pragma unroll 8
+  for (int w = 0; w < 32; ++w) {
+    const int64_t sw = s_warp[w];
+    wpre += w < wid ? sw : 0;
+    total += sw;
+  }
+  if (b < nblk) R[b] = (int32_t)(wpre + inc - v);    // in-group prefix < 2^31
+  if (t == 0) GS[blockIdx.x] = total;
+}
+
+// exclusive prefix of tile b: its in-group prefix + the sums of the groups
+// before it (one warp; every lane returns it)
+__device__ __forceinline__ int64_t tile_prefix(const int32_t* __restrict__ R,
+                                               const int64_t* __restrict__ GS, int64_t b) {
+  const int lane = threadIdx.x & 31;
+  const int64_t g = b >> 10;
+  int64_t acc = 0;
+  for (int64_t q = lane; q < g; q += 32) acc += GS[q];
+#pragma unroll
+  for (int d = 16; d >= 1; d >>= 1) acc += __shfl_xor_sync(kFull, acc, d);
+  return acc + R[b];
+}
+
+// one tile (kScanTile orders from b0) scanned from `prefix` and written to OFF
+// (256 threads; shared-memory transpose so the int64 stores leave coalesced).
+// Returns the tile's total on every thread.
+// The prefix comes from get_prefix() (called by every thread after the tile's
+// loads are issued; it must publish to *s_pre from one thread), read after the
+// block scan's barrier, so its loads overlap the tile's.
+template <typename GetPrefix>
+__device__ __forceinline__ int64_t scan_write_tile(const uint8_t* __restrict__ NM, int64_t N,
+                                                   int64_t* __restrict__ OFF, int64_t b0,
+                                                   GetPrefix&& get_prefix, int64_t* s_pre,
+                                                   bool vec, int64_t* s_warp, int64_t* s_out) {
   constexpr int RS = kScanPer + 1;           // padded row: conflict-free row writes
-  __shared__ int64_t s_out[kThreads * RS];
-  const int64_t b0 = (int64_t)blockIdx.x * kScanTile;
-  const int64_t prefix = OFF[b0];            // written by pass 2 (b0 < N always)
+  const int t = threadIdx.x & (kThreads - 1);
   int v[kScanPer];
-  scan_load16(NM, N, b0 + (int64_t)threadIdx.x * kScanPer, vec, v);
+  scan_load16(NM, N, b0 + (int64_t)t * kScanPer, vec, v);
+  get_prefix();
   int sum = 0;
 #pragma unroll
   for (int k = 0; k < kScanPer; ++k) sum += v[k];
   int64_t total;
-  int64_t p = prefix + block_excl_scan(sum, s_warp, total);
-  // transpose through shared memory so the int64 stores leave coalesced
+  const int64_t local = block_excl_scan(sum, s_warp, total);
+  int64_t p = *s_pre + local;
 #pragma unroll
   for (int k = 0; k < kScanPer; ++k) {
-    s_out[threadIdx.x * RS + k] = p;
+    s_out[t * RS + k] = p;
     p += v[k];
   }
   __syncthreads();
   const int cnt = (int)min((int64_t)kScanTile, N - b0);
-  for (int k = threadIdx.x; k < cnt; k += kThreads)
+  for (int k = t; k < cnt; k += kThreads)
     OFF[b0 + k] = s_out[(k / kScanPer) * RS + (k % kScanPer)];
+  __syncthreads();                           // s_warp / s_out reuse
+  return total;
+}
+
+__global__ void __launch_bounds__(kThreads)
+offsets_tiles_kernel(const uint8_t* __restrict__ NM, int64_t N, int64_t* __restrict__ OFF,
+                     const int32_t* __restrict__ R, const int64_t* __restrict__ GS, bool vec) {
+  __shared__ int64_t s_warp[kThreads / 32];
+  __shared__ int64_t s_out[kThreads * (kScanPer + 1)];
+  __shared__ int64_t s_pre;
+  const int64_t b = blockIdx.x;
+  scan_write_tile(NM, N, OFF, b * kScanTile, [&] {
+    if (threadIdx.x < 32) {
+      const int64_t p = tile_prefix(R, GS, b);
+      if (threadIdx.x == 0) s_pre = p;
+    }
+  }, &s_pre, vec, s_warp, s_out);
+}
+
+// tiles tfirst..nblk-1 (their outputs overlap R): prefixes first, then writes
+__global__ void __launch_bounds__(kThreads)
+offsets_tail_kernel(const uint8_t* __restrict__ NM, int64_t N, int64_t* __restrict__ OFF,
+                    const int32_t* __restrict__ R, const int64_t* __restrict__ GS,
+                    int64_t tfirst, int64_t nblk, bool vec) {
+  extern __shared__ int64_t s_pre[];         // nblk - tfirst prefixes
+  __shared__ int64_t s_warp[kThreads / 32];
+  __shared__ int64_t s_out[kThreads * (kScanPer + 1)];
+  const int wid = threadIdx.x >> 5;
+  for (int64_t q = wid; q < nblk - tfirst; q += kThreads / 32) {
+    const int64_t p = tile_prefix(R, GS, tfirst + q);
+    if ((threadIdx.x & 31) == 0) s_pre[q] = p;
+  }
+  __syncthreads();
+  int64_t last = 0;
+  for (int64_t b = tfirst; b < nblk; ++b)
+    last = s_pre[b - tfirst] + scan_write_tile(NM, N, OFF, b * kScanTile, [] {}, &s_pre[b - tfirst],
+                                               vec, s_warp, s_out);
+  if (threadIdx.x == 0) OFF[N] = last;       // grand total
 }
 
 template <typename T, int NB, int EPL, int CPE, int MINB, int WT = kThreads>
@@ -558,12 +628,30 @@ boys_status ragged_offsets_base(const uint8_t* nmax_dev, int64_t N, int64_t* off
                                 cudaStream_t s) {
   if (N == 0) return cuda_status(cudaMemsetAsync(offsets_dev, 0, sizeof(int64_t), s));
   const int64_t nblk = (N + kScanTile - 1) / kScanTile;
+  const int64_t ngrp = (nblk + 1023) / 1024;
   if (nblk > INT32_MAX) return BOYS_E_ARG;
   const bool vec = (reinterpret_cast<uintptr_t>(nmax_dev) & 15) == 0;
-  offsets_totals_kernel<<<(unsigned)nblk, kThreads, 0, s>>>(nmax_dev, N, offsets_dev, vec);
-  offsets_blocks_kernel<<<1, 1024, 0, s>>>(N, nblk, offsets_dev);
-  offsets_tiles_kernel<<<(unsigned)nblk, kThreads, 0, s>>>(nmax_dev, N, offsets_dev, vec);
-  g_launches.fetch_add(3, std::memory_order_relaxed);
+  // parked at the array's tail: group sums GS (int64), then the tile totals R
+  // (int32: a tile's total is at most 4096 * 256)
+  const int64_t park = ngrp + (nblk + 1) / 2;            // int64 words, <= N + 1
+  int64_t* GS = offsets_dev + (N + 1 - park);
+  int32_t* R = reinterpret_cast<int32_t*>(GS + ngrp);
+  // first tile overlapping the parked words (at least the last tile: it also writes OFF[N])
+  const int64_t tfirst = min((N + 1 - park) / kScanTile, nblk - 1);
+  const int64_t ntail = nblk - tfirst;
+  if (ntail * (int64_t)sizeof(int64_t) > 12 * 1024) return BOYS_E_ARG;    // N > ~2^33
+  offsets_totals_kernel<<<(unsigned)((nblk + kTotTiles - 1) / kTotTiles), kThreads, 0, s>>>(
+      nmax_dev, N, R, nblk, vec);
+  offsets_groups_kernel<<<(unsigned)ngrp, 1024, 0, s>>>(nblk, R, GS);
+  int launches = 3;
+  if (tfirst > 0) {
+    offsets_tiles_kernel<<<(unsigned)tfirst, kThreads, 0, s>>>(nmax_dev, N, offsets_dev, R, GS,
+                                                                vec);
+    ++launches;
+  }
+  offsets_tail_kernel<<<1, kThreads, ntail * sizeof(int64_t), s>>>(nmax_dev, N, offsets_dev, R,
+                                                                     GS, tfirst, nblk, vec);
+  g_launches.fetch_add(launches, std::memory_order_relaxed);
   return cuda_status(cudaGetLastError());
 }
 

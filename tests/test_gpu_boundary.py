@@ -161,8 +161,8 @@ def test_ragged_strided_offsets_made_contiguous(oracle):
     assert np.array_equal(got.cpu().numpy().view(np.int64), ref.view(np.int64))
 
 
-@pytest.mark.parametrize("N", [1, 15, 16, 17, 4095, 4096, 4097, 8192 + 5, (1 << 20) + 3,
-                               3 * 4096 * 1024 + 1])
+@pytest.mark.parametrize("N", [1, 15, 16, 17, 4095, 4096, 4097, 8192, 8192 + 5, (1 << 20) + 3,
+                               4096 * 4096, 4096 * 4096 + 4096 * 3 - 1, 3 * 4096 * 1024 + 1])
 def test_offsets_scan_sizes(N):
     g = torch.Generator(device="cuda").manual_seed(N)
     nm = torch.randint(0, 37, (N + 1,), generator=g, device="cuda", dtype=torch.uint8)
@@ -180,10 +180,11 @@ def test_offsets_scan_full_cfg4_size():
     ref = torch.zeros((1 << 27) + 1, dtype=torch.int64, device="cuda")
     torch.cumsum(nm.to(torch.int64) + 1, 0, out=ref[1:])
     assert torch.equal(got, ref)
-    # no allocation per call: the launch issues the scan's three kernels only
+    # no allocation per call: the launch issues the scan's four kernels only
+    # (totals, totals scan, tiles, the tiles overlapping the parked totals)
     l0 = _lib.launch_count()
     ragged_offsets(nm)
-    assert _lib.launch_count() - l0 == 3
+    assert _lib.launch_count() - l0 == 4
 
 
 @pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
