@@ -222,7 +222,7 @@ boys_status boys_eval_dense_host(boys_dtype dtype, int n_max, const void* x_host
   if (e != cudaSuccess) return cuda_status(e);
   const size_t es = dsize(dtype);
   const int W = n_max + 1;
-  const int64_t chunk = N < host_chunk() ? N : host_chunk();
+  const int64_t chunk = N < kHostChunk ? N : kHostChunk;
   HostPipe* p = nullptr;
   st = pipe_get(dev, chunk * es, chunk * W * es, &p);
   if (st != BOYS_OK) return st;
@@ -292,7 +292,7 @@ boys_status boys_eval_ragged_host(boys_dtype dtype, const void* x_host, const ui
     }
   }
   const size_t es = dsize(dtype);
-  const int64_t chunk = N < host_chunk() ? N : host_chunk();
+  const int64_t chunk = N < kHostChunk ? N : kHostChunk;
   const int64_t nchunks = (N + chunk - 1) / chunk;
   // per-chunk domain slots; x/n/offsets buffers sized once for the chunk
   for (int k = 0; k < 2; ++k) {

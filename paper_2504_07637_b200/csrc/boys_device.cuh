@@ -15,17 +15,7 @@ namespace boys {
 
 constexpr int kThreads = 256;   // points per tile == threads per block
 constexpr int kRaggedFastOrders = 16;
-#ifndef BOYS_SOA_MINB
-#define BOYS_SOA_MINB 4   // SoA resident-block target (register budget 64/thread)
-#endif
 constexpr unsigned kFull = 0xffffffffu;
-#ifndef BOYS_PAIR_MINB_SMALL
-#define BOYS_PAIR_MINB_SMALL 5   // paired SoA kernel, n <= 1: resident-block target (47 registers; cfg1 9.27 us vs 9.50 / 9.71 / 9.65 / 9.75 for 6 / 4 / 3 / 8)
-#endif
-#ifndef BOYS_FAST_CR
-#define BOYS_FAST_CR 0   // 1: ragged chunks use the branch-free CR rcp/sqrt fast paths (A/B: f64 1.88 vs 1.83 ms, slower)
-#endif
-
 
 __device__ __forceinline__ void flag_domain(int64_t* dom, int64_t i) {
   if (dom) atomicMin(reinterpret_cast<unsigned long long*>(dom), (unsigned long long)i);

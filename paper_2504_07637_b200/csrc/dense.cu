@@ -246,7 +246,7 @@ dense_aos_pair_kernel(const T* __restrict__ X, int64_t N, T* __restrict__ out,
 template <typename T, int n, bool AOS, int NBUF, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB)
 dense_kernel(const T* __restrict__ X, int64_t N, T* __restrict__ out, T* __restrict__ expx,
-             int64_t* __restrict__ dom, int64_t index_base, bool bulk_ok, bool soa_bulk) {
+             int64_t* __restrict__ dom, int64_t index_base, bool bulk_ok) {
   constexpr int W = n + 1;
   constexpr int TILE_ELEMS = kThreads * W;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -260,39 +260,17 @@ dense_kernel(const T* __restrict__ X, int64_t N, T* __restrict__ out, T* __restr
     const int64_t i = i0 + tid;
     const bool in = i < N;
     // (loading the next tile's x one iteration ahead measured slower:
-    // SoA 77% vs 84%, AoS 86% vs 94% of HBM, tools/ab/ab25.sh)
+    // SoA 77% vs 84%, AoS 86% vs 94% of HBM)
     const T x = in ? ldg_nc(X + i) : T(0);
     bool ok = valid_x(x);
     if (in && !ok) flag_domain(dom, index_base + i);
     ok = ok || !in;   // tail lanes evaluate x = 0 quietly
     if constexpr (!AOS) {
-      if (soa_bulk) {
-        // [n+1][256] tile in shared memory, one bulk copy per order row
-        T* buf = sbase + (it % NBUF) * TILE_ELEMS;
-        if (tid == 0) bulk_wait_read<NBUF - 1>();
-        __syncthreads();
-        T t = eval_point_stream<T, n>(x, ok, [&](int m, T v) { buf[m * kThreads + tid] = v; });
-        if (expx && in) __stcs(expx + i, t);
-        const int64_t cnt = (N - i0) < kThreads ? (N - i0) : kThreads;
-        if (cnt == kThreads) {
-          fence_proxy_async_smem();
-          __syncthreads();
-          if (tid < W) bulk_store(out + (int64_t)tid * N + i0, buf + tid * kThreads,
-                                  kThreads * sizeof(T));
-        } else {
-          __syncthreads();
-          for (int k = tid; k < W * kThreads; k += kThreads) {
-            const int m = k / kThreads, j = k % kThreads;
-            if (j < cnt) __stcs(out + (int64_t)m * N + i0 + j, buf[k]);
-          }
-        }
-      } else {
-        T* o = out + i;
-        T t = eval_point_stream<T, n>(x, ok, [&](int m, T v) {
-          if (in) __stcs(o + (int64_t)m * N, v);
-        });
-        if (expx && in) __stcs(expx + i, t);
-      }
+      T* o = out + i;
+      T t = eval_point_stream<T, n>(x, ok, [&](int m, T v) {
+        if (in) __stcs(o + (int64_t)m * N, v);
+      });
+      if (expx && in) __stcs(expx + i, t);
     } else {
       T* buf = sbase + (it % NBUF) * TILE_ELEMS;
       // the slot went to the bulk engine NBUF tiles ago: wait until it was read
@@ -313,148 +291,104 @@ dense_kernel(const T* __restrict__ X, int64_t N, T* __restrict__ out, T* __restr
       }
     }
   }
-  if (AOS || soa_bulk) {
-    if (tid < (AOS ? 1 : W)) bulk_wait_all();
-  }
+  if (AOS && tid == 0) bulk_wait_all();
 }
 
-template <typename T, int n, bool AOS, int NBUF, int MINB>
-static boys_status launch_dense_k(const T* x, int64_t N, T* out, T* expx, int64_t* dom,
-                                  int64_t base, cudaStream_t s) {
-  auto k = dense_kernel<T, n, AOS, NBUF, MINB>;
-  // SoA bulk rows need every row start 16-byte aligned: N * sizeof(T) % 16 == 0
-  const bool soa_bulk = !AOS && soa_tma() && (N * (int64_t)sizeof(T)) % 16 == 0 &&
-                        (reinterpret_cast<uintptr_t>(out) % 16) == 0;
-  size_t smem = (AOS || soa_bulk) ? (size_t)NBUF * kThreads * (n + 1) * sizeof(T) : 0;
-  // the dynamic-smem opt-in is per function *per device*: remember each device
-  static std::atomic<uint64_t> attr_mask{0};
-  {
-    const int smem_max = (int)((size_t)NBUF * kThreads * (n + 1) * sizeof(T));
-    boys_status st = opt_in_smem(k, smem_max, attr_mask);
-    if (st != BOYS_OK) return st;
-  }
-  int64_t ntiles = (N + kThreads - 1) / kThreads;
-  bool bulk_ok = (reinterpret_cast<uintptr_t>(out) % 16) == 0;
-  // Grid: persistent (SMs x resident blocks) or one block per tile, chosen
-  // by same-box measurement (tools/ab/ab29.sh, ab30.sh; graph-replayed
-  // streams at 2^20..2^24 points): one block per tile wins for f64 SoA at
-  // n <= 5 and n >= 11 (n=0: 143 vs 154 us, n=16: 398 vs 471 us at 2^24),
-  // persistent for f64 SoA n = 6..10 (n=8: 265 vs 282 us), for f32 SoA and for
-  // AoS (whose double-buffered bulk stores need the loop).  BOYS_GRID_TILES=1/2
-  // forces one or the other.
-  int grid = blocks_for(k, smem, ntiles);
-  const int gt = grid_tiles();
-  const bool per_tile = gt == 1 || (gt == 0 && !AOS && !soa_bulk && sizeof(T) == 8 &&
-                                    (n <= 5 || n >= 11));
-  if (per_tile && ntiles <= (int64_t)1 << 30) grid = (int)ntiles;
-  if (pdl()) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, k, x, N, out, expx, dom, base, bulk_ok, soa_bulk);
-    if (e != cudaSuccess) return cuda_status(e);
-  } else {
-    k<<<grid, kThreads, smem, s>>>(x, N, out, expx, dom, base, bulk_ok, soa_bulk);
-  }
+// ---------------------------------------------------------------------------
+// launches.  Every dense kernel is launched with programmatic stream
+// serialization (PDL): its blocks wait for the previous grid at entry
+// (pdl_wait_and_release), so only the launch and prologue overlap the
+// previous kernel's tail.  Kernel and grid choices below are fixed rules, each
+// chosen by same-box B200 measurement (DESIGN.md section 6 records the A/B
+// numbers; the losing variants were removed).
+// ---------------------------------------------------------------------------
+template <typename K, typename... Args>
+static boys_status launch_pdl(K kernel, int grid, size_t smem, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, args...);
+  if (e != cudaSuccess) return cuda_status(e);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cuda_status(cudaGetLastError());
 }
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+// one block per tile (falls back to a persistent grid past 2^30 tiles)
+template <typename K>
+static int per_tile_grid(K kernel, size_t smem, int64_t ntiles) {
+  return ntiles <= ((int64_t)1 << 30) ? (int)ntiles : blocks_for(kernel, smem, ntiles);
+}
 
+// one-point kernel: SoA fallback (odd N / unaligned buffers) and AoS rows that
+// do not fit the paired / register-row kernels
+template <typename T, int n, bool AOS, int NBUF, int MINB>
+static boys_status launch_dense_k(const T* x, int64_t N, T* out, T* expx, int64_t* dom,
+                                  int64_t base, cudaStream_t s) {
+  auto k = dense_kernel<T, n, AOS, NBUF, MINB>;
+  const size_t smem = AOS ? (size_t)NBUF * kThreads * (n + 1) * sizeof(T) : 0;
+  // the dynamic-smem opt-in is per function *per device*: remember each device
+  static std::atomic<uint64_t> attr_mask{0};
+  if (AOS) {
+    boys_status st = opt_in_smem(k, (int)smem, attr_mask);
+    if (st != BOYS_OK) return st;
+  }
+  const int64_t ntiles = (N + kThreads - 1) / kThreads;
+  const bool bulk_ok = aligned16(out);
+  // one block per tile for f64 SoA at n <= 5 and n >= 11 (n=0: 143 vs 154 us,
+  // n=16: 398 vs 471 us at 2^24); persistent otherwise (f64 SoA n=6..10: n=8
+  // 265 vs 282 us; f32 SoA; AoS, whose double-buffered bulk stores need the loop)
+  const bool per_tile = !AOS && sizeof(T) == 8 && (n <= 5 || n >= 11);
+  const int grid = per_tile ? per_tile_grid(k, smem, ntiles) : blocks_for(k, smem, ntiles);
+  return launch_pdl(k, grid, smem, s, x, N, out, expx, dom, base, bulk_ok);
+}
+
+// SoA, two adjacent points per thread: one block per 512-point tile for every
+// f64 order (n=8: 230 vs 266 us, n=12: 314 vs 371 us at 2^24) and f32 n >= 6;
+// persistent for f32 n < 6 (n=4: 82 vs 90 us)
 template <typename T, int n>
 static boys_status launch_soa_pair(const T* x, int64_t N, T* out, T* expx, int64_t* dom,
                                    int64_t base, cudaStream_t s) {
-#ifndef BOYS_PAIR_MINB_HIGH
-#define BOYS_PAIR_MINB_HIGH BOYS_SOA_MINB   // orders >= 11 (A/B: 3 blocks / 80 regs no better, ab45)
-#endif
-  constexpr int MINB = n <= 1 ? BOYS_PAIR_MINB_SMALL : (n >= 11 ? BOYS_PAIR_MINB_HIGH : BOYS_SOA_MINB);   // two chains: 8 blocks would spill at n = 0
+  // resident-block targets: two chains would spill at 8 blocks for n <= 1
+  // (5: 47 registers, cfg1 9.27 us vs 9.50 / 9.71 / 9.65 / 9.75 for 6 / 4 / 3 / 8)
+  constexpr int MINB = n <= 1 ? 5 : 4;
   auto k = dense_soa_pair_kernel<T, n, MINB>;
   const int64_t ntiles = (N + 2 * kThreads - 1) / (2 * kThreads);
-  int grid = blocks_for(k, 0, ntiles);
-  const int gt = grid_tiles();
-  if ((gt == 1 || (gt == 0 && soa_pair_per_tile(sizeof(T) == 8, n))) && ntiles <= ((int64_t)1 << 30))
-    grid = (int)ntiles;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = 0;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = pdl() ? 1 : 0;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, k, x, N, out, expx, dom, base);
-  if (e != cudaSuccess) return cuda_status(e);
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-  return cuda_status(cudaGetLastError());
+  const bool per_tile = sizeof(T) == 8 || n >= 6;
+  const int grid = per_tile ? per_tile_grid(k, 0, ntiles) : blocks_for(k, 0, ntiles);
+  return launch_pdl(k, grid, 0, s, x, N, out, expx, dom, base);
 }
 
-#ifndef BOYS_AOS_VEC_P
-#define BOYS_AOS_VEC_P 0     // A/B override of the register-row kernel's points per thread
-#endif
-#ifndef BOYS_AOS_VEC_MINB
-#define BOYS_AOS_VEC_MINB 4
-#endif
-#ifndef BOYS_QUAD_MINB
-#define BOYS_QUAD_MINB 4   // 59 registers at n = 0 (3 / 2: 66 / 68, slower, ab49)
-#endif
+// SoA, four adjacent points per thread (n <= 3: f64 2^24 n=0 113 vs 123 us,
+// n=1 122 vs 135, n=3 152 vs 167; f32 n <= 2 9-13% faster), one block per
+// 1024-point tile (persistent: cfg1 10.8 vs 9.25 us), 4 resident blocks (59-64
+// registers; 3 / 2: slower), branch-free correctly rounded div/sqrt/rcp.
 template <typename T, int n>
 static boys_status launch_soa_quad(const T* x, int64_t N, T* out, T* expx, int64_t* dom,
                                    int64_t base, cudaStream_t s) {
-  static const int fast = env_int("BOYS_QUAD_FASTCR", 1);
-  auto k = fast ? dense_soa_quad_kernel<T, n, BOYS_QUAD_MINB, true>
-                : dense_soa_quad_kernel<T, n, BOYS_QUAD_MINB, false>;
+  auto k = dense_soa_quad_kernel<T, n, 4, true>;
   const int64_t ntiles = (N + 4 * kThreads - 1) / (4 * kThreads);
-  // one block per 1024-point tile (BOYS_GRID_TILES=2: persistent grid, slower: cfg1 10.8 vs 9.25 us)
-  const int grid = (grid_tiles() != 2 && ntiles <= ((int64_t)1 << 30)) ? (int)ntiles
-                                                                        : blocks_for(k, 0, ntiles);
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = 0;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = pdl() ? 1 : 0;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, k, x, N, out, expx, dom, base);
-  if (e != cudaSuccess) return cuda_status(e);
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-  return cuda_status(cudaGetLastError());
+  return launch_pdl(k, per_tile_grid(k, 0, ntiles), 0, s, x, N, out, expx, dom, base);
 }
 
+// AoS rows of 2..4 values kept in registers, P points per thread, direct
+// 16-byte stores, one block per tile
 template <typename T, int n, int P>
 static boys_status launch_aos_vec(const T* x, int64_t N, T* out, T* expx, int64_t* dom,
                                   int64_t base, cudaStream_t s) {
-  auto k = dense_aos_vec_kernel<T, n, P, BOYS_AOS_VEC_MINB>;
+  auto k = dense_aos_vec_kernel<T, n, P, 4>;
   const int64_t ntiles = (N + P * kThreads - 1) / (P * kThreads);
-  const int grid = ntiles <= ((int64_t)1 << 30) ? (int)ntiles : blocks_for(k, 0, ntiles);
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = 0;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = pdl() ? 1 : 0;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, k, x, N, out, expx, dom, base);
-  if (e != cudaSuccess) return cuda_status(e);
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-  return cuda_status(cudaGetLastError());
+  return launch_pdl(k, per_tile_grid(k, 0, ntiles), 0, s, x, N, out, expx, dom, base);
 }
 
+// AoS, two points per thread with the [512][n+1] tile staged and bulk-stored
 template <typename T, int n>
 static boys_status launch_aos_pair(const T* x, int64_t N, T* out, T* expx, int64_t* dom,
                                    int64_t base, cudaStream_t s) {
@@ -467,63 +401,39 @@ static boys_status launch_aos_pair(const T* x, int64_t N, T* out, T* expx, int64
   boys_status st = opt_in_smem(k, (int)smem, attr_mask);
   if (st != BOYS_OK) return st;
   const int64_t ntiles = (N + 2 * kThreads - 1) / (2 * kThreads);
-  const bool bulk_ok = (reinterpret_cast<uintptr_t>(out) % 16) == 0;
-  const int grid = blocks_for(k, smem, ntiles);
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = pdl() ? 1 : 0;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, k, x, N, out, expx, dom, base, bulk_ok);
-  if (e != cudaSuccess) return cuda_status(e);
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-  return cuda_status(cudaGetLastError());
+  return launch_pdl(k, blocks_for(k, smem, ntiles), smem, s, x, N, out, expx, dom, base,
+                    aligned16(out));
 }
 
 template <typename T, int n, bool AOS>
 static boys_status launch_dense_t(const T* x, int64_t N, T* out, T* expx, int64_t* dom,
                                   int64_t base, cudaStream_t s) {
+  const bool al = aligned16(x) && aligned16(out) && (!expx || aligned16(expx));
   if constexpr (!AOS) {
-    constexpr bool fits2 = 2 * kThreads * (n + 1) * sizeof(T) <= 80 * 1024;
-    if (soa_tma()) return launch_dense_k<T, n, false, (fits2 ? 2 : 1), 4>(x, N, out, expx, dom, base, s);
-    if constexpr (n <= 1) {          // small orders: register budget for 6 or 8 blocks/SM
-      if (soa_small_minb() == 6) return launch_dense_k<T, n, false, 1, 6>(x, N, out, expx, dom, base, s);
+    if constexpr (n <= 3) {
+      if (N % 4 == 0 && al) return launch_soa_quad<T, n>(x, N, out, expx, dom, base, s);
     }
-    if constexpr (n <= 5) {
-      if (soa_quad(n) && N % 4 == 0 && aligned16(x) && aligned16(out) && (!expx || aligned16(expx)))
-        return launch_soa_quad<T, n>(x, N, out, expx, dom, base, s);
-    }
-    if (soa_pair() && N % 2 == 0 && aligned16(x) && aligned16(out) && (!expx || aligned16(expx)))
-      return launch_soa_pair<T, n>(x, N, out, expx, dom, base, s);
-    return launch_dense_k<T, n, false, 1, (n <= 1 ? 8 : BOYS_SOA_MINB)>(x, N, out, expx, dom, base, s);
+    if (N % 2 == 0 && al) return launch_soa_pair<T, n>(x, N, out, expx, dom, base, s);
+    return launch_dense_k<T, n, false, 1, (n <= 1 ? 8 : 4)>(x, N, out, expx, dom, base, s);
   } else {
-    if constexpr (n >= 1 && n <= 6) {
-      // register rows + direct 16-byte stores: default for n = 1, 2 and f32
-      // n = 3; the staged kernels win from n = 4 (f64 from n = 3).  ab56/ab57,
-      // 2^24: n=1 f64 128.6 vs 158.2 us, f32 63.4 vs 91.2; n=2 f64 149.2 vs
-      // 168.1, f32 82.9 vs 96.2; f32 n=3 88.1 vs 97.8; f64 n=3 180 vs 173.
-      constexpr int P = BOYS_AOS_VEC_P > 0 ? BOYS_AOS_VEC_P
-                        : (n == 1 || (n == 2 && sizeof(T) == 8)) ? 4 : 2;
-      constexpr bool deflt = n <= 2 || (n == 3 && sizeof(T) == 4);
-      if (aos_vec(deflt) && N % P == 0 && aligned16(x) && aligned16(out) &&
-          (!expx || aligned16(expx)))
-        return launch_aos_vec<T, n, P>(x, N, out, expx, dom, base, s);
+    if constexpr (n >= 1 && n <= 3) {
+      // register rows + direct 16-byte stores for n = 1, 2 and f32 n = 3 (2^24:
+      // n=1 f64 128.6 vs 158.2 us, f32 63.4 vs 91.2; n=2 f64 149.2 vs 168.1,
+      // f32 82.9 vs 96.2; f32 n=3 88.1 vs 97.8); the staged kernels win from
+      // f64 n = 3 (180 vs 173 us)
+      constexpr int P = (n == 1 || (n == 2 && sizeof(T) == 8)) ? 4 : 2;
+      constexpr bool use = n <= 2 || sizeof(T) == 4;
+      if (use && N % P == 0 && al) return launch_aos_vec<T, n, P>(x, N, out, expx, dom, base, s);
     }
-    if constexpr (2 * 2 * kThreads * (n + 1) * sizeof(T) <= 110 * 1024) {
-      constexpr bool small_tile = 2 * 2 * kThreads * (n + 1) * sizeof(T) <= 72 * 1024;
-      if (aos_pair(small_tile)) return launch_aos_pair<T, n>(x, N, out, expx, dom, base, s);
-    }
-    // double-buffer the AoS tile while two tiles fit in ~80 KB (n <= 18 in f64)
+    // paired AoS where the double-buffered 512-point tile allows 3 blocks/SM
+    // (f64 n <= 8, every f32 order: f64 n=2 168 vs 196 us, n=8 241 vs 248;
+    // f32 n=8 116 vs 144, n=16 197 vs 217; slower for f64 n >= 10)
+    if constexpr (2 * 2 * kThreads * (n + 1) * sizeof(T) <= 72 * 1024)
+      return launch_aos_pair<T, n>(x, N, out, expx, dom, base, s);
+    // one point per thread, the AoS tile double-buffered while two tiles fit
+    // in ~80 KB (f64 n <= 18)
     constexpr bool fits2 = 2 * kThreads * (n + 1) * sizeof(T) <= 80 * 1024;
-    if (fits2 && aos_nbuf() == 2)
-      return launch_dense_k<T, n, true, (fits2 ? 2 : 1), 4>(x, N, out, expx, dom, base, s);
-    if (aos_minb() == 6) return launch_dense_k<T, n, true, 1, 6>(x, N, out, expx, dom, base, s);
-    return launch_dense_k<T, n, true, 1, 4>(x, N, out, expx, dom, base, s);
+    return launch_dense_k<T, n, true, (fits2 ? 2 : 1), 4>(x, N, out, expx, dom, base, s);
   }
 }
 

@@ -593,24 +593,13 @@ static boys_status launch_ragged(const void* x, const uint8_t* nm, const int64_t
     // (order-sorted warp super-chunks were measured slower: 2.90 / 3.79 ms vs 2.42)
     // elements per lane: measured best 3 (f64: 1.95 ms vs 2.27 / 1.97 / 2.05
     // for 1 / 2 / 4) and 4 (f32: 1.14 ms vs 1.26 / 1.16 / 1.36 for 2 / 3 / 6)
-#ifndef BOYS_RAGGED_CPE
-#define BOYS_RAGGED_CPE 12   // staged values per element (chunk output capacity)
-#endif
-#ifndef BOYS_RAGGED_EPL64
-#define BOYS_RAGGED_EPL64 3
-#endif
-#ifndef BOYS_RAGGED_EPL32
-#define BOYS_RAGGED_EPL32 4
-#endif
-    constexpr int EPL = sizeof(T) == 8 ? BOYS_RAGGED_EPL64 : BOYS_RAGGED_EPL32;
-    // (8 instead of 12 staged values per element, or a 3-blocks/SM register
-    // bound, measured no better: 1.96 / 2.08 ms f64)
-    // (f64, 2 elements per lane with 10 staged values each, 24 warps/SM:
-    // 1.88 ms -- within 1%, but overflows to the slow path from order 10)
-    // (128-thread blocks, also with a 96-register bound and 8 staged values per
-    // element for 20 resident warps, measured slower: f64 1.84-2.36 vs 1.78 ms,
-    // f32 0.94-1.00 vs 0.94 ms, tools/ab/ab39.sh)
-    boys_status st = launch_chunks<T, NB, EPL, BOYS_RAGGED_CPE, 0>(x, nm, off, N, out, dom, s);
+    // elements per lane: measured best 3 (f64: 1.95 ms vs 2.27 / 1.97 / 2.05
+    // for 1 / 2 / 4) and 4 (f32: 1.14 ms vs 1.26 / 1.16 / 1.36 for 2 / 3 / 6);
+    // 12 staged values per element (8: 1.96 ms f64; 2 elements x 10 values,
+    // 24 warps/SM: within 1% but overflows to the slow path from order 10;
+    // 128-thread blocks / 96-register bound: f64 1.84-2.36 vs 1.78 ms)
+    constexpr int EPL = sizeof(T) == 8 ? 3 : 4, CPE = 12;
+    boys_status st = launch_chunks<T, NB, EPL, CPE, 0>(x, nm, off, N, out, dom, s);
     if (st != BOYS_OK) return st;
   }
   g_launches.fetch_add(1, std::memory_order_relaxed);

@@ -10,9 +10,9 @@
 
 namespace boys {
 
-#ifndef BOYS_SPLIT_SOA_MINB
-#define BOYS_SPLIT_SOA_MINB 3   // SoA split: 3 resident blocks (80 regs); unbounded (134 regs, 1 block) was 2x slower (ab55)
-#endif
+// SoA split: 3 resident blocks (80 registers); unbounded (134 registers, 1
+// block) was 2x slower
+constexpr int kSplitSoaMinB = 3;
 
 // ---------------------------------------------------------------------------
 // split kernel (eval_with_split): F_m for m <= nbar equals a
@@ -95,7 +95,7 @@ __device__ __forceinline__ void split_point(T x_in, bool ok, int nbar_rt, Put&& 
 }
 
 template <typename T, int n, int NBAR, bool AOS, int NBUF>
-__global__ void __launch_bounds__(kThreads, AOS ? 4 : BOYS_SPLIT_SOA_MINB)
+__global__ void __launch_bounds__(kThreads, AOS ? 4 : kSplitSoaMinB)
 split_kernel(const T* __restrict__ X, int64_t N, int nbar, T* __restrict__ out,
              int64_t* __restrict__ dom, bool bulk_ok) {
   constexpr int W = n + 1;
