@@ -336,12 +336,19 @@ def eval_with_split(n: int, n_bar: int, x, table=None, layout: str = "soa", chec
     return out if isinstance(x, torch.Tensor) and x.is_cuda else out.cpu().numpy()
 
 
-def ragged_offsets(n_max: torch.Tensor) -> torch.Tensor:
-    """Exclusive prefix sum of n_i + 1 (N+1 entries), computed on the device."""
+def ragged_offsets(n_max: torch.Tensor, out: torch.Tensor = None) -> torch.Tensor:
+    """Exclusive prefix sum of n_i + 1 (N+1 entries), computed on the device.
+    ``out``: optional preallocated contiguous int64 tensor of N+1 entries."""
     nm = n_max.contiguous().reshape(-1)
     if nm.dtype != torch.uint8 or not nm.is_cuda:
         raise ValueError("n_max must be a CUDA uint8 tensor")
-    off = torch.empty(nm.numel() + 1, dtype=torch.int64, device=nm.device)
+    if out is None:
+        off = torch.empty(nm.numel() + 1, dtype=torch.int64, device=nm.device)
+    else:
+        if (out.dtype != torch.int64 or out.numel() != nm.numel() + 1 or out.device != nm.device
+                or not out.is_contiguous()):
+            raise ValueError("out must be a contiguous int64 tensor of N+1 entries on n_max's device")
+        off = out.reshape(-1)
     with torch.cuda.device(nm.device):
         L.check(L.load().boys_ragged_offsets(_ptr(nm), nm.numel(), _ptr(off),
                                              C.c_void_p(_stream_ptr(nm.device))))
