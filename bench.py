@@ -762,6 +762,85 @@ def e2e_dense(cfg_name, steps, dev):
                                     "(chunked H2D / kernel / D2H pipeline)"}
 
 
+def hermite_ops(L: int) -> int:
+    """Algorithmic FP64 ops per quartet of the fused consumer (same weights as
+    roofline.ops_per_point: div/rcp 8, sqrt 7, every other DP op 1): the Boys
+    evaluation at order L (Table I N of that order), the pair geometry, the
+    (-2a)^n F_n products, the Hermite recurrences and the prefactor."""
+    from paper_2504_07637_b200 import roofline as R
+    ops = R.ops_per_point(L, 8)
+    ops += 3 + 1 + 1 + 8 + 3 + 1              # X, Y, Z; p+q; pq; /; r2 (mul + 2 fma); x
+    ops += 2 * (L + 1)                        # R0_k = pw_k F_k, pw_{k+1} = pw_k (-2a)
+    for n in range(L - 1, -1, -1):            # recurrences: fma + mul, or one mul
+        for s in range(L - n, 0, -1):
+            for t in range(s, -1, -1):
+                for u in range(s - t, -1, -1):
+                    v = s - t - u
+                    ops += 2 if (t >= 2 or (t == 0 and u >= 2) or (t == 0 and u == 0 and v >= 2)) else 1
+    ops += 1 + 7 + 1 + 8 + 1 + 1              # den = (pq) sqrt(p+q); pref
+    ops += (L + 1) * (L + 2) * (L + 3) // 6   # pref * R
+    return ops
+
+
+def hermite_line(ctx, steps, warmup, hbm_peak, fp64_peak, L=4, npairs=4096):
+    """The fused consumer as a bench line: McMurchie-Davidson
+    Hermite Coulomb integrals for npairs x npairs primitive quartets at order
+    L, F_0..F_L consumed in registers; device-resident pair data, CUDA events."""
+    from paper_2504_07637_b200 import hermite_coulomb, workloads as W
+    dev = ctx.dev
+    bra = W.shell_pairs(npairs, seed=21, chunk=ctx.rank, device=dev)
+    ket = W.shell_pairs(npairs, seed=22, chunk=ctx.rank, device=dev)
+    NH = (L + 1) * (L + 2) * (L + 3) // 6
+    # two output buffers, alternating (4.7 GB each): no launch rewrites lines
+    # the previous one left dirty in L2
+    outs = [torch.empty((npairs, npairs, NH), dtype=torch.float64, device=dev) for _ in range(2)]
+    for k in range(warmup):
+        hermite_coulomb(L, bra, ket, out=outs[k % 2], check=False)
+    ctx.sync()
+    l0 = launch_count(ctx)
+    a = ctx.mark()
+    for k in range(steps):
+        hermite_coulomb(L, bra, ket, out=outs[k % 2], check=False)
+    b = ctx.mark()
+    out = outs[(steps - 1) % 2]
+    ctx.sync()
+    launches = launch_count(ctx) - l0
+    ms = ctx.ms(a, b) / steps
+    nq = npairs * npairs
+    bytes_q = NH * 8
+    gbs = bytes_q * nq / (ms * 1e-3) / 1e9
+    ops = hermite_ops(L)
+    tops = ops * nq / (ms * 1e-3)
+    # bit-exactness against the CPU restatement on a 64 x 64 corner
+    from oracle import oracle as O
+    ref, bad = O.hermite(L, bra[:64].cpu().numpy(), ket[:64].cpu().numpy())
+    got = out[:64, :64].cpu().numpy()
+    same = bool(bad == -1 and np.array_equal(got.view(np.int64), ref.view(np.int64)))
+    t_b, t_o = bytes_q * nq / (hbm_peak * 1e9), ops * nq / fp64_peak if fp64_peak else 0.0
+    bound = "fp64" if t_o > t_b else "hbm"
+    roof = ({"bound": "hbm", "achieved": round(gbs, 1), "peak": hbm_peak, "unit": "GB/s",
+             "frac": round(gbs / hbm_peak, 4)} if bound == "hbm" else
+            {"bound": "fp64", "achieved": round(tops / 1e12, 3), "peak": round(fp64_peak / 1e12, 3),
+             "unit": "TDPop/s", "frac": round(tops / fp64_peak, 4)})
+    roof.update({"traffic": None, "algorithmic_bytes_per_launch": bytes_q * nq,
+                 "bytes_per_quartet": bytes_q, "fp64_ops_per_quartet": ops,
+                 "fp64_ops_frac": round(tops / fp64_peak, 4) if fp64_peak else None,
+                 "launch_ms": round(ms, 4),
+                 "note": ("write-only stream: it can exceed the copy test (read + write) that "
+                          "defines the peak; ncu of this launch: 4.64 GB DRAM writes in 0.670 ms "
+                          "= 6.93 TB/s, 84.6% of the DRAM peak ncu reports "
+                          "(profiles/r02_hermite_ncu.md)")})
+    return {"value": ctx.sum(nq / (ms * 1e-3)), "unit": "quartets/s",
+            "F_values_consumed_per_s": ctx.sum(nq * (L + 1) / (ms * 1e-3)),
+            "steps": steps, "n_gpus": ctx.ws, "ms_per_step": ms, "scaling": "weak",
+            "gpu_launches": launches, "roofline": roof,
+            "accuracy": {"bit_identical_to_port": same, "compared_quartets": 64 * 64},
+            "workload": (f"fused consumer: McMurchie-Davidson Hermite Coulomb integrals R_tuv, "
+                         f"t+u+v <= {L} ({NH} per quartet), {npairs} x {npairs} primitive "
+                         f"pair quartets (cfg4-like exponents), F_0..F_{L} in registers, never "
+                         f"written; output [{npairs}][{npairs}][{NH}] fp64, two buffers alternating")}
+
+
 def e2e_ragged(wl, steps):
     """Host-buffer ragged path through the public API (C-ABI
     boys_eval_ragged_host): pinned host x and orders in, pinned values out."""
@@ -906,7 +985,7 @@ def main():
 
     # the other BASELINE configurations (same protocol, fewer steps)
     extras_list = (args.extras.split(",") if args.extras else
-                   (["cfg1", "cfg1_l2flush", "cfg2", "cfg4", "cfg4f32", "cfg5", "split"]
+                   (["cfg1", "cfg1_l2flush", "cfg2", "cfg4", "cfg4f32", "cfg5", "split", "hermite"]
                     if ctx.ws == 1 else ["cfg5"]))
     if not args.no_extras:
         extras = {}
@@ -920,8 +999,19 @@ def main():
         # off the GPU's critical path; 512 MiB working set, each batch cold
         # in L2 when its launch starts); (b) one batch, L2 flushed before every
         # launch (also evicts code and __constant__ tables)
-        plan = {"cfg1": ("cfg1", 32, "graph"), "cfg1_l2flush": ("cfg1", 1, "flush")}
+        # cfg2 (1.3 GB per launch): two distinct batches per step, outputs
+        # alternating, so dirty L2 lines of one launch are written back during
+        # the next instead of being overwritten in L2 (which would flatter HBM)
+        plan = {"cfg1": ("cfg1", 32, "graph"), "cfg1_l2flush": ("cfg1", 1, "flush"),
+                "cfg2": ("cfg2", 2, None)}
         for key in extras_list:
+            if key == "hermite":
+                try:
+                    extras[key] = hermite_line(ctx, min(args.steps, 50), args.warmup, hbm_peak,
+                                               fp64_peak)
+                except Exception as ex:  # noqa: BLE001
+                    extras[key] = {"error": str(ex)[:300]}
+                continue
             name, rot, fl = plan.get(key, (key, 1, None))
             if name == args.config:
                 continue
@@ -934,11 +1024,15 @@ def main():
                 v2 = ctx.sum(w2.values_per_step * k) / r2["secs"]
                 if fl == "flush":
                     note = "flushed (1 GiB memset) before every launch; kernel time only"
-                elif rot > 1:
+                elif rot > 1 and fl == "graph":
                     note = (f"{rot} distinct batches per step, launched back to back as one "
                             "CUDA-graph replay "
                             f"({rot} x {w2.bytes_per_point * w2.points_per_step / rot / 2**20:.0f} MiB "
                             "working set > L2)")
+                elif rot > 1:
+                    note = (f"{rot} distinct batches per step with their own outputs "
+                            f"({w2.bytes_per_point * w2.points_per_step / rot / 2**30:.2f} GiB per "
+                            "launch, > L2; no output is rewritten while its dirty lines sit in L2)")
                 else:
                     note = "exceeds L2"
                 if name == "split":

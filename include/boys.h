@@ -21,6 +21,8 @@
  *   order check (refmath.py:104-108, MAX_ORDER :41)       BOYS_E_ORDER / boys_max_order
  *   eval_batch with host arrays (the CPU caller's view)   boys_eval_dense_host
  *   ragged work lists with host arrays                   boys_eval_ragged_host
+ *   downstream integral code (SURVEY     boys_hermite_coulomb
+ *       8(f)#4: fused consumer of F_m)
  *
  * Conventions
  *   - Device pointers are caller-owned, 16-byte aligned for x/out, and the work
@@ -143,6 +145,19 @@ boys_status boys_eval_split_table(const boys_table* table, int n, int n_bar, con
  * one launch; the caller initialises *err_dev (0.0) and gathers it across ranks. */
 boys_status boys_shard_error(boys_dtype dtype, const void* vals_dev, const int64_t* pos_dev,
                              const double* gold_dev, int64_t K, double* err_dev, void* stream);
+
+/* Fused consumer (the downstream integral code SPEC.md:16, 353
+ * names as the caller): McMurchie-Davidson Hermite Coulomb integrals for every
+ * (bra pair i, ket pair j), F_0..F_L evaluated in registers and consumed there:
+ *   a = p q/(p+q), x = a |P-Q|^2, R^{(n)}_{000} = (-2a)^n F_n(x), Helgaker's
+ *   recurrences to R^{(0)}_{tuv}, t+u+v <= L;
+ *   out[(i Nk + j) NH + k] = 2 pi^{5/2} / (p q sqrt(p+q)) K_i K_j R_{tuv},
+ * NH = (L+1)(L+2)(L+3)/6 in the canonical order (s = t+u+v ascending, then t
+ * descending, then u descending).  Pair records are 5 doubles: p, Px, Py, Pz, K.
+ * 0 <= L <= 4 (BOYS_E_ORDER otherwise); fp64; stream-ordered.  dom_dev: first
+ * quartet with an invalid x or p, q <= 0 (their outputs are NaN). */
+boys_status boys_hermite_coulomb(int L, const double* bra_dev, int64_t Nb, const double* ket_dev,
+                                 int64_t Nk, double* out_dev, int64_t* dom_dev, void* stream);
 
 /* Number of kernel launches issued by this library in this process. */
 int64_t boys_launch_count(void);

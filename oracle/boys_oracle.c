@@ -299,6 +299,82 @@ int64_t boys_oracle_split(const void* t, int n, int nbar, const void* x, int64_t
   return first_bad == INT64_MAX ? -1 : first_bad;
 }
 
+/* Fused consumer: McMurchie-Davidson Hermite Coulomb
+ * integrals pref * R^{(0)}_{tuv}, t+u+v <= L, for every (bra pair i, ket pair
+ * j); pair records are 5 doubles (p, Px, Py, Pz, K).  The operation sequence
+ * of csrc/hermite.cu (Helgaker's recurrences, in place, level n = L-1..0 in
+ * decreasing order s = t+u+v), in C with explicit fma:
+ *   a = (p q)/(p + q); x = a * fma(Z,Z, fma(Y,Y, X*X)); F_0..F_L(x) as point_f64;
+ *   R^{(k)}_{000} = ((-2a)^k, by repeated products) * F_k;
+ *   R_{t,u,v} = fma(X, R_{t-1,u,v}, (t-1) * R_{t-2,u,v})  (t > 0; first term
+ *   alone at t = 1), else the u then v recurrence; pref = ((2 pi^{5/2}) /
+ *   ((p q) sqrt(p+q))) K_i K_j.  Output [Nb][Nk][NH].  Returns the first
+ *   offending quartet index (x invalid or p, q <= 0), or -1. */
+static int herm_count(int L) { return (L + 1) * (L + 2) * (L + 3) / 6; }
+static int herm_index(int t, int u, int v) {
+  const int s = t + u + v;
+  int before = 0;
+  for (int tp = s; tp > t; --tp) before += s - tp + 1;
+  return herm_count(s - 1) + before + (s - t - u);
+}
+
+int64_t boys_oracle_hermite(const void* tab, int L, const double* bra, int64_t Nb,
+                            const double* ket, int64_t Nk, double* out) {
+  const oracle_table* ot = tab;
+  if (L < 0 || L > 8) return -2;
+  const int NH = herm_count(L);
+  int64_t first_bad = INT64_MAX;
+  const double two_pi52 = 0x1.17e50a9dc6553p+5;   /* RN(2 pi^{5/2}) */
+#pragma omp parallel for schedule(static) reduction(min : first_bad)
+  for (int64_t q = 0; q < Nb * Nk; ++q) {
+    const double* b = bra + 5 * (q / Nk);
+    const double* k = ket + 5 * (q % Nk);
+    const double p = b[0], qq = k[0];
+    const double X = b[1] - k[1], Y = b[2] - k[2], Z = b[3] - k[3];
+    const double pq = p + qq;
+    const double a = (p * qq) / pq;
+    const double r2 = fma(Z, Z, fma(Y, Y, X * X));
+    const double x = a * r2;
+    double F[MAXN + 1], R[165], R0[MAXN + 1] = {0};
+    int ok = point_f64(&ot->t64, L, x, F, NULL);
+    if (!(p > 0.0 && qq > 0.0)) {
+      ok = 0;
+      for (int m = 0; m <= L; ++m) F[m] = NAN;
+    }
+    const double m2a = -2.0 * a;
+    double pw = 1.0;
+    for (int m = 0; m <= L; ++m) {
+      R0[m] = pw * F[m];
+      pw = pw * m2a;
+    }
+    R[0] = R0[L];
+    for (int n = L - 1; n >= 0; --n) {
+      for (int s = L - n; s >= 1; --s)
+        for (int t = s; t >= 0; --t)
+          for (int u = s - t; u >= 0; --u) {
+            const int v = s - t - u;
+            double val;
+            if (t > 0)
+              val = t >= 2 ? fma(X, R[herm_index(t - 1, u, v)], (double)(t - 1) * R[herm_index(t - 2, u, v)])
+                           : X * R[herm_index(t - 1, u, v)];
+            else if (u > 0)
+              val = u >= 2 ? fma(Y, R[herm_index(0, u - 1, v)], (double)(u - 1) * R[herm_index(0, u - 2, v)])
+                           : Y * R[herm_index(0, u - 1, v)];
+            else
+              val = v >= 2 ? fma(Z, R[herm_index(0, 0, v - 1)], (double)(v - 1) * R[herm_index(0, 0, v - 2)])
+                           : Z * R[herm_index(0, 0, v - 1)];
+            R[herm_index(t, u, v)] = val;
+          }
+      R[0] = R0[n];
+    }
+    const double den = (p * qq) * sqrt(pq);
+    const double pref = ((two_pi52 / den) * b[4]) * k[4];
+    for (int m = 0; m < NH; ++m) out[q * NH + m] = pref * R[m];
+    if (!ok && q < first_bad) first_bad = q;
+  }
+  return first_bad == INT64_MAX ? -1 : first_bad;
+}
+
 /* Q~_n(x) alone (eval_qtilde), for SPEC.md:295-297 checks. */
 void boys_oracle_qtilde(const void* t, int n, const void* x, int64_t N, void* out) {
   const oracle_table* ot = t;

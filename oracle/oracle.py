@@ -80,6 +80,9 @@ def lib():
         L.boys_oracle_qtilde.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_void_p]
         L.boys_oracle_expneg.argtypes = [C.c_int, C.c_void_p, C.c_int64, C.c_void_p]
         L.boys_oracle_threads.restype = C.c_int
+        L.boys_oracle_hermite.restype = C.c_int64
+        L.boys_oracle_hermite.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int64,
+                                          C.c_void_p, C.c_int64, C.c_void_p]
         _lib = L
     return _lib
 
@@ -145,6 +148,19 @@ def split(n: int, nbar: int, x, layout: str = "soa", table_path=None):
     out = np.empty((n + 1, N) if layout == "soa" else (N, n + 1), dtype=x.dtype)
     bad = lib().boys_oracle_split(table(x.dtype, table_path), n, nbar, _ptr(x), N, _ptr(out),
                                   0 if layout == "soa" else 1)
+    return out, bad
+
+
+def hermite(L: int, bra, ket):
+    """Fused consumer restatement: pref * R_{tuv} (t+u+v <= L) for every
+    (bra pair, ket pair); pair records (p, Px, Py, Pz, K).  Returns
+    (values [Nb][Nk][NH], first_bad)."""
+    bra = np.ascontiguousarray(bra, dtype=np.float64).reshape(-1, 5)
+    ket = np.ascontiguousarray(ket, dtype=np.float64).reshape(-1, 5)
+    NH = (L + 1) * (L + 2) * (L + 3) // 6
+    out = np.empty((bra.shape[0], ket.shape[0], NH))
+    bad = lib().boys_oracle_hermite(table(np.float64), L, _ptr(bra), bra.shape[0], _ptr(ket),
+                                    ket.shape[0], _ptr(out))
     return out, bad
 
 

@@ -7,7 +7,7 @@ kernels behind the C ABI in include/boys.h.
 
 Public API (mirrors the reference's SPEC'd ``kernel`` module):
     boys, boys_ragged, ragged_offsets, eval_batch, eval_fn, eval_with_split,
-    EvalRequest, EvalResult, max_order
+    EvalRequest, EvalResult, max_order; and the fused consumer hermite_coulomb
 """
 
 from .kernel import (  # noqa: F401
@@ -18,6 +18,7 @@ from .kernel import (  # noqa: F401
     eval_batch,
     eval_fn,
     eval_with_split,
+    hermite_coulomb,
     max_order,
     ragged_offsets,
 )

@@ -24,6 +24,7 @@ EXPORTS = (
     "boys_launch_count", "boys_status_str", "boys_last_cuda_error",
     "boys_table_checksum", "boys_table_row_bytes", "boys_table_create", "boys_table_destroy",
     "boys_table_max_order", "boys_eval_dense_table", "boys_eval_split_table", "boys_shard_error",
+    "boys_hermite_coulomb",
 )
 
 _lock = threading.Lock()
@@ -86,6 +87,8 @@ def load(build_if_missing: bool = True) -> C.CDLL:
         L.boys_eval_split_table.argtypes = [vp, i32, i32, vp, i64, vp, i32, vp, vp]
         L.boys_shard_error.restype = i32
         L.boys_shard_error.argtypes = [i32, vp, vp, vp, i64, vp, vp]
+        L.boys_hermite_coulomb.restype = i32
+        L.boys_hermite_coulomb.argtypes = [i32, vp, i64, vp, i64, vp, vp, vp]
         L.boys_launch_count.restype = i64
         L.boys_status_str.restype = C.c_char_p
         L.boys_status_str.argtypes = [i32]

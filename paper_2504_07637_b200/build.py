@@ -13,7 +13,7 @@ LIB = PKG / "libboys.so"
 PROBE_LIB = PKG / "libboys_probe.so"
 # translation units of libboys (compiled in parallel, linked into one .so)
 UNITS = [CSRC / "dense.cu", CSRC / "ragged.cu", CSRC / "split.cu", CSRC / "table.cu",
-         CSRC / "shard.cu", CSRC / "abi.cu"]
+         CSRC / "shard.cu", CSRC / "hermite.cu", CSRC / "abi.cu"]
 SOURCES = UNITS + [CSRC / "boys_device.cuh", CSRC / "boys_launch.h", CSRC / "boys_eval.cuh",
                    CSRC / "boys_tables.inc", PKG.parent / "include" / "boys.h"]
 

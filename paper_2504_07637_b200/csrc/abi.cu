@@ -202,6 +202,19 @@ boys_status boys_shard_error(boys_dtype dtype, const void* vals_dev, const int64
   return shard_error_base(dtype, vals_dev, pos_dev, gold_dev, K, err_dev, (cudaStream_t)stream);
 }
 
+boys_status boys_hermite_coulomb(int L, const double* bra_dev, int64_t Nb, const double* ket_dev,
+                                 int64_t Nk, double* out_dev, int64_t* dom_dev, void* stream) {
+  if (L < 0 || L > 4) return BOYS_E_ORDER;
+  if (Nb < 0 || Nk < 0) return BOYS_E_ARG;
+  if (Nb == 0 || Nk == 0) return BOYS_OK;
+  if (!bra_dev || !ket_dev || !out_dev) return BOYS_E_ARG;
+  if ((reinterpret_cast<uintptr_t>(bra_dev) | reinterpret_cast<uintptr_t>(ket_dev) |
+       reinterpret_cast<uintptr_t>(out_dev)) % sizeof(double))
+    return BOYS_E_ALIGN;
+  if (Nb > (int64_t(1) << 62) / Nk) return BOYS_E_ARG;
+  return hermite_base(L, bra_dev, Nb, ket_dev, Nk, out_dev, dom_dev, (cudaStream_t)stream);
+}
+
 boys_status boys_domain_result(const int64_t* dom_dev, int64_t* first_bad, void* stream) {
   if (!dom_dev || !first_bad) return BOYS_E_ARG;
   cudaStream_t s = (cudaStream_t)stream;

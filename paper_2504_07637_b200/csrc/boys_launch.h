@@ -97,6 +97,8 @@ boys_status eval_ragged_base(boys_dtype dtype, const void* x, const uint8_t* nm,
                              const int64_t* off, int64_t N, void* out, int64_t* dom,
                              cudaStream_t s);
 boys_status ragged_offsets_base(const uint8_t* nm, int64_t N, int64_t* off, cudaStream_t s);
+boys_status hermite_base(int L, const double* bra, int64_t Nb, const double* ket, int64_t Nk,
+                         double* out, int64_t* dom, cudaStream_t s);
 boys_status shard_error_base(boys_dtype dtype, const void* vals, const int64_t* pos,
                              const double* gold, int64_t K, double* err, cudaStream_t s);
 

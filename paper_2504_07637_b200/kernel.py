@@ -454,3 +454,41 @@ def boys_ragged(x: torch.Tensor, n_max: torch.Tensor, offsets: torch.Tensor = No
                              f"supported maximum {mx}")
         _domain_error(xf, first)
     return out, offsets
+
+
+def hermite_coulomb(lmax: int, bra: torch.Tensor, ket: torch.Tensor, *, out: torch.Tensor = None,
+                    check: bool = True) -> torch.Tensor:
+    """Fused consumer of F_m (SPEC.md:16, 353 name downstream
+    integral code as the caller): McMurchie-Davidson Hermite Coulomb integrals
+    for every (bra pair, ket pair), with F_0..F_L evaluated and consumed in
+    registers (include/boys.h boys_hermite_coulomb).  lmax = L of the formulas.
+
+    bra: [Nb, 5], ket: [Nk, 5] float64 CUDA tensors of pair records
+    (p, Px, Py, Pz, K).  Returns [Nb, Nk, NH] with NH = (L+1)(L+2)(L+3)/6:
+    2 pi^{5/2} / (p q sqrt(p+q)) K_i K_j R_{tuv}(a = pq/(p+q), P-Q), t+u+v <= L,
+    canonical order (t+u+v ascending, then t descending, then u descending)."""
+    if not isinstance(lmax, (int, np.integer)) or not 0 <= lmax <= 4:
+        raise ValueError(f"lmax must be an integer in [0, 4], got {lmax!r}")
+    for name, t in (("bra", bra), ("ket", ket)):
+        if (not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float64
+                or t.dim() != 2 or t.shape[1] != 5):
+            raise ValueError(f"{name} must be a float64 CUDA tensor of shape [N, 5]")
+    if bra.device != ket.device:
+        raise ValueError("bra and ket must be on the same device")
+    bra, ket = bra.contiguous(), ket.contiguous()
+    NH = (lmax + 1) * (lmax + 2) * (lmax + 3) // 6
+    shape = (bra.shape[0], ket.shape[0], NH)
+    if out is None:
+        out = torch.empty(shape, dtype=torch.float64, device=bra.device)
+    elif (tuple(out.shape) != shape or out.dtype != torch.float64 or out.device != bra.device
+          or not out.is_contiguous()):
+        raise ValueError(f"out must be a contiguous float64 tensor of shape {shape}")
+    dom = torch.full((1,), -1, dtype=torch.int64, device=bra.device) if check else None
+    with torch.cuda.device(bra.device):
+        L.check(L.load().boys_hermite_coulomb(int(lmax), _ptr(bra), bra.shape[0], _ptr(ket), ket.shape[0],
+                                              _ptr(out), _ptr(dom), C.c_void_p(_stream_ptr(bra.device))))
+    if check and int(dom.item()) >= 0:
+        q = int(dom.item())
+        raise ValueError(f"invalid pair data (x not finite/non-negative, or exponent <= 0) at "
+                         f"quartet {q} (bra {q // ket.shape[0]}, ket {q % ket.shape[0]})")
+    return out

@@ -138,6 +138,23 @@ def cfg4f32_batch(n=1 << 27, seed=4, chunk=0, device="cpu"):
     return x[keep].to(torch.float32), nm[keep]
 
 
+def shell_pairs(n, seed=6, chunk=0, device="cpu"):
+    """Primitive shell-pair records for the fused consumer (hermite_coulomb):
+    [n, 5] float64 (p, Px, Py, Pz, K) from two primitives with exponents
+    log-uniform [0.05, 50], centre A uniform in a 20-bohr cube and B within
+    1.5 bohr of it per axis (pairs that survive Schwarz-type screening):
+    p = a + b, P = (aA + bB)/p, K = exp(-ab/p |A-B|^2)."""
+    g = _gen(seed, chunk, device)
+    e = _logu(g, 2 * n, 0.05, 50.0, device).view(2, n)
+    A = _u(g, 3 * n, 0.0, 20.0, device).view(3, n)
+    B = A + _u(g, 3 * n, -1.5, 1.5, device).view(3, n)
+    a, b = e[0], e[1]
+    p = a + b
+    P = (a * A + b * B) / p
+    K = torch.exp(-(a * b / p) * ((A - B) ** 2).sum(0))
+    return torch.stack([p, P[0], P[1], P[2], K], dim=1).contiguous()
+
+
 def config_x(name: str, n: int = None, seed: int = None, chunk: int = 0, device="cpu"):
     """Dense-config inputs (cfg1/2/3/5) with the config's default size/seed."""
     fn = {"cfg1": cfg1_x, "cfg2": cfg2_x, "cfg3": cfg3_x, "cfg5": cfg5_x}[name]
