@@ -220,7 +220,7 @@ __device__ __forceinline__ void eval_multi_stream(const T (&xin)[P], const bool 
 #pragma unroll
   for (int j = 0; j < P; ++j) {
     x[j] = ok[j] ? xin[j] : bad;
-    t[j] = exp_neg_clamped(x[j]);
+    t[j] = FAST ? exp_neg_select(x[j]) : exp_neg_clamped(x[j]);
     below = below || (ok[j] && x[j] < R.z);
   }
   const bool any_below = __any_sync(kFull, below);

@@ -230,7 +230,7 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
       const bool ok = in[e] && xok[e];
       xs[e] = ok ? x[e] : A::nan();                // NaN propagates through the tail
       const T xe = ok ? x[e] : T(0);
-      t[e] = exp_neg_clamped(xe);
+      t[e] = exp_neg_select(xe);
       zc[e] = S.zc[n[e]];
       // deferred to the warp queue: below the cut-off (Q~ needed) and, in
       // fp32, above x_up (upward ladder)

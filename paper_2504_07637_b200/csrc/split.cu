@@ -26,7 +26,7 @@ __device__ __forceinline__ void split_point(T x_in, bool ok, int nbar_rt, Put&& 
   using A = Ar<T>;
   const int nbar = NBAR >= 0 ? NBAR : nbar_rt;      // warp-uniform
   const T x = ok ? x_in : A::nan();                  // NaN through every step
-  const T t = exp_neg_clamped(x);
+  const T t = exp_neg_select(x);
   const T tx = A::add(x, x);
   {
     // order n: seed, recursion n-1 .. nbar+1
