@@ -74,6 +74,26 @@ __device__ __forceinline__ void psts(bool p, float* a, float v) {
 
 
 
+// Shared-memory row stride for a staged [points][W] AoS tile.  The 32 lanes
+// write element m of 32 consecutive rows together; a row width that is a
+// multiple of 16 elements puts them all in one or two banks (f64 n=15 ran at
+// 49.6% of HBM, n=31 at 60.0%, f32 n=15 at 60.7%), so those rows are padded by
+// one element and the tile leaves through coalesced thread stores instead of
+// one bulk copy (86.8 / 87.5 / 73.2%).  Other widths keep the dense layout and
+// the bulk copy: padding every even width measured worse (f64 n=9: 68.6 vs
+// 91.7%), the thread copy-out costing more than the milder conflicts.
+template <int W>
+struct RowStride {
+  static constexpr bool padded = W % 16 == 0;
+  static constexpr int value = padded ? W + 1 : W;
+};
+template <typename T, int W, int WS>
+__device__ __forceinline__ void copy_out_rows(T* __restrict__ dst, const T* buf, int64_t cnt,
+                                              int tid, int nthreads) {
+  for (int64_t k = tid; k < cnt * W; k += nthreads)
+    __stcs(dst + k, buf[(k / W) * WS + (k % W)]);
+}
+
 // F_0..F_n for one point, handed to put(m, value) in the order n, n-1, .., 0
 // (then, for lanes past x_up, 0..n again with the upward values).  Returns
 // e^{-x}.  `ok` = x in the domain; other lanes produce NaN.  Lanes only

@@ -192,9 +192,9 @@ __global__ void __launch_bounds__(kThreads, MINB)
 dense_aos_pair_kernel(const T* __restrict__ X, int64_t N, T* __restrict__ out,
                       T* __restrict__ expx, int64_t* __restrict__ dom, int64_t index_base,
                       bool bulk_ok) {
-  constexpr int W = n + 1;
+  constexpr int W = n + 1, WS = RowStride<W>::value;
   constexpr int TILE = 2 * kThreads;
-  constexpr int TILE_ELEMS = TILE * W;
+  constexpr int TILE_ELEMS = TILE * WS;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   T* sbase = reinterpret_cast<T*>(smem_raw);
   const int tid = threadIdx.x;
@@ -215,8 +215,8 @@ dense_aos_pair_kernel(const T* __restrict__ X, int64_t N, T* __restrict__ out,
     T* buf = sbase + (it % NBUF) * TILE_ELEMS;
     if (tid == 0) bulk_wait_read<NBUF - 1>();
     __syncthreads();
-    T* ra = buf + tid * W;
-    T* rb = buf + (kThreads + tid) * W;
+    T* ra = buf + tid * WS;
+    T* rb = buf + (kThreads + tid) * WS;
     T ta, tb;
     eval_pair_stream<T, n>(
         xa, xb, oka, okb, ta, tb,
@@ -227,14 +227,13 @@ dense_aos_pair_kernel(const T* __restrict__ X, int64_t N, T* __restrict__ out,
       if (inb) __stcs(expx + ib, tb);
     }
     const int64_t cnt = (N - i0) < TILE ? (N - i0) : TILE;
-    if (bulk_ok && cnt == TILE) {
+    if (!RowStride<W>::padded && bulk_ok && cnt == TILE) {
       fence_proxy_async_smem();
       __syncthreads();
       if (tid == 0) bulk_store(out + i0 * W, buf, TILE_ELEMS * sizeof(T));
     } else {
       __syncthreads();
-      T* dst = out + i0 * W;
-      for (int k = tid; k < cnt * W; k += kThreads) __stcs(dst + k, buf[k]);
+      copy_out_rows<T, W, WS>(out + i0 * W, buf, cnt, tid, kThreads);
     }
   }
   if (tid == 0) bulk_wait_all();
@@ -247,8 +246,8 @@ template <typename T, int n, bool AOS, int NBUF, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB)
 dense_kernel(const T* __restrict__ X, int64_t N, T* __restrict__ out, T* __restrict__ expx,
              int64_t* __restrict__ dom, int64_t index_base, bool bulk_ok) {
-  constexpr int W = n + 1;
-  constexpr int TILE_ELEMS = kThreads * W;
+  constexpr int W = n + 1, WS = RowStride<W>::value;
+  constexpr int TILE_ELEMS = kThreads * WS;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   T* sbase = reinterpret_cast<T*>(smem_raw);
   const int tid = threadIdx.x;
@@ -276,18 +275,17 @@ dense_kernel(const T* __restrict__ X, int64_t N, T* __restrict__ out, T* __restr
       // the slot went to the bulk engine NBUF tiles ago: wait until it was read
       if (tid == 0) bulk_wait_read<NBUF - 1>();
       __syncthreads();
-      T* row = buf + tid * W;
+      T* row = buf + tid * WS;
       T t = eval_point_stream<T, n>(x, ok, [&](int m, T v) { row[m] = v; });
       if (expx && in) __stcs(expx + i, t);
       const int64_t cnt = (N - i0) < kThreads ? (N - i0) : kThreads;
-      if (bulk_ok && cnt == kThreads) {
+      if (!RowStride<W>::padded && bulk_ok && cnt == kThreads) {
         fence_proxy_async_smem();
         __syncthreads();
         if (tid == 0) bulk_store(out + i0 * W, buf, TILE_ELEMS * sizeof(T));
       } else {
         __syncthreads();
-        T* dst = out + i0 * W;
-        for (int k = tid; k < cnt * W; k += kThreads) __stcs(dst + k, buf[k]);
+        copy_out_rows<T, W, WS>(out + i0 * W, buf, cnt, tid, kThreads);
       }
     }
   }
@@ -333,7 +331,7 @@ template <typename T, int n, bool AOS, int NBUF, int MINB>
 static boys_status launch_dense_k(const T* x, int64_t N, T* out, T* expx, int64_t* dom,
                                   int64_t base, cudaStream_t s) {
   auto k = dense_kernel<T, n, AOS, NBUF, MINB>;
-  const size_t smem = AOS ? (size_t)NBUF * kThreads * (n + 1) * sizeof(T) : 0;
+  const size_t smem = AOS ? (size_t)NBUF * kThreads * RowStride<n + 1>::value * sizeof(T) : 0;
   // the dynamic-smem opt-in is per function *per device*: remember each device
   static std::atomic<uint64_t> attr_mask{0};
   if (AOS) {
@@ -392,8 +390,8 @@ static boys_status launch_aos_vec(const T* x, int64_t N, T* out, T* expx, int64_
 template <typename T, int n>
 static boys_status launch_aos_pair(const T* x, int64_t N, T* out, T* expx, int64_t* dom,
                                    int64_t base, cudaStream_t s) {
-  constexpr size_t tile_bytes = (size_t)2 * kThreads * (n + 1) * sizeof(T);
-  constexpr int NBUF = 2 * tile_bytes <= 110 * 1024 ? 2 : 1;
+  constexpr size_t tile_bytes = (size_t)2 * kThreads * RowStride<n + 1>::value * sizeof(T);
+  constexpr int NBUF = (2 * tile_bytes <= 110 * 1024 && !RowStride<n + 1>::padded) ? 2 : 1;
   constexpr int MINB = NBUF * tile_bytes <= 72 * 1024 ? 3 : 2;
   auto k = dense_aos_pair_kernel<T, n, NBUF, MINB>;
   const size_t smem = NBUF * tile_bytes;
@@ -432,7 +430,9 @@ static boys_status launch_dense_t(const T* x, int64_t N, T* out, T* expx, int64_
       return launch_aos_pair<T, n>(x, N, out, expx, dom, base, s);
     // one point per thread, the AoS tile double-buffered while two tiles fit
     // in ~80 KB (f64 n <= 18)
-    constexpr bool fits2 = 2 * kThreads * (n + 1) * sizeof(T) <= 80 * 1024;
+    // (padded rows leave through synchronous thread stores: one buffer)
+    constexpr bool fits2 = 2 * kThreads * (n + 1) * sizeof(T) <= 80 * 1024 &&
+                           !RowStride<n + 1>::padded;
     return launch_dense_k<T, n, true, (fits2 ? 2 : 1), 4>(x, N, out, expx, dom, base, s);
   }
 }

@@ -98,8 +98,8 @@ template <typename T, int n, int NBAR, bool AOS, int NBUF>
 __global__ void __launch_bounds__(kThreads, AOS ? 4 : kSplitSoaMinB)
 split_kernel(const T* __restrict__ X, int64_t N, int nbar, T* __restrict__ out,
              int64_t* __restrict__ dom, bool bulk_ok) {
-  constexpr int W = n + 1;
-  constexpr int TILE_ELEMS = kThreads * W;
+  constexpr int W = n + 1, WS = RowStride<W>::value;
+  constexpr int TILE_ELEMS = kThreads * WS;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   T* sbase = reinterpret_cast<T*>(smem_raw);
   const int tid = threadIdx.x;
@@ -120,17 +120,16 @@ split_kernel(const T* __restrict__ X, int64_t N, int nbar, T* __restrict__ out,
       T* buf = sbase + (it % NBUF) * TILE_ELEMS;
       if (tid == 0) bulk_wait_read<NBUF - 1>();
       __syncthreads();
-      T* row = buf + tid * W;
+      T* row = buf + tid * WS;
       split_point<T, n, NBAR>(x, ok, nbar, [&](int m, T v) { row[m] = v; });
       const int64_t cnt = (N - i0) < kThreads ? (N - i0) : kThreads;
-      if (bulk_ok && cnt == kThreads) {
+      if (!RowStride<W>::padded && bulk_ok && cnt == kThreads) {
         fence_proxy_async_smem();
         __syncthreads();
         if (tid == 0) bulk_store(out + i0 * W, buf, TILE_ELEMS * sizeof(T));
       } else {
         __syncthreads();
-        T* dst = out + i0 * W;
-        for (int k = tid; k < cnt * W; k += kThreads) __stcs(dst + k, buf[k]);
+        copy_out_rows<T, W, WS>(out + i0 * W, buf, cnt, tid, kThreads);
       }
     } else {
       T* o = out + i;
@@ -145,7 +144,7 @@ split_kernel(const T* __restrict__ X, int64_t N, int nbar, T* __restrict__ out,
 template <typename T, int n, bool AOS>
 static boys_status launch_split_t(const T* x, int64_t N, int nbar, T* out, int64_t* dom,
                                   cudaStream_t s) {
-  constexpr bool fits2 = 2 * kThreads * (n + 1) * sizeof(T) <= 80 * 1024;
+  constexpr bool fits2 = 2 * kThreads * (n + 1) * sizeof(T) <= 80 * 1024 && !RowStride<n + 1>::padded;
   constexpr int NBUF = (AOS && fits2) ? 2 : 1;
   // compile-time lower order for the common pairs: n_bar = n - 1 (one more
   // order: "a few more bits") and n_bar = n / 2
@@ -156,7 +155,7 @@ static boys_status launch_split_t(const T* x, int64_t N, int nbar, T* out, int64
   auto k = var == 0   ? split_kernel<T, n, NB1, AOS, NBUF>
            : var == 1 ? split_kernel<T, n, NB2, AOS, NBUF>
                       : split_kernel<T, n, -1, AOS, NBUF>;
-  const size_t smem = AOS ? (size_t)NBUF * kThreads * (n + 1) * sizeof(T) : 0;
+  const size_t smem = AOS ? (size_t)NBUF * kThreads * RowStride<n + 1>::value * sizeof(T) : 0;
   static std::atomic<uint64_t> attr_mask[3];         // per kernel variant, per device
   if (AOS) {
     boys_status st = opt_in_smem(k, (int)smem, attr_mask[var]);
