@@ -280,7 +280,7 @@ __device__ __forceinline__ void eval_multi_stream(const T (&xin)[P], const bool 
   for (int j = 0; j < P; ++j) tout[j] = ok[j] ? t[j] : bad;
 }
 
-template <typename T, int n, typename Put, typename Put1>
+template <typename T, int n, bool FAST = false, typename Put, typename Put1>
 __device__ __forceinline__ void eval_pair_stream(T xa, T xb, bool oka, bool okb, T& ta_out,
                                                  T& tb_out, Put&& put, Put1&& put1) {
   using A = Ar<T>;
@@ -292,11 +292,13 @@ __device__ __forceinline__ void eval_pair_stream(T xa, T xb, bool oka, bool okb,
   bool below = false, up = false;
 #pragma unroll
   for (int j = 0; j < 2; ++j) {
-    t[j] = exp_neg_clamped(x[j]);
+    t[j] = FAST ? exp_neg_select(x[j]) : exp_neg_clamped(x[j]);
     below = below || (ok[j] && x[j] < R.z);
   }
   const bool any_below = __any_sync(kFull, below);
-  {
+  if constexpr (FAST && sizeof(T) == 8) {
+    seed_multi_fast<n, 2>(x, t, any_below, cur);
+  } else {
 #pragma unroll
     for (int j = 0; j < 2; ++j) cur[j] = seed<T, n>(x[j], t[j], any_below);
   }

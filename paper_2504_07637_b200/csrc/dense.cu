@@ -12,6 +12,15 @@
 
 namespace boys {
 
+// Where the multi-point kernels take the branch-free correctly rounded
+// div/sqrt/rcp (seed_multi_fast), by same-box order sweep at 2^24 (f64): the
+// AoS register-row kernel (n=1: 0.1232 -> 0.1141 ms, n=2: 0.1365 -> 0.1248)
+// and the SoA pair kernel from n = 11 (1-2% faster); not the SoA pair kernel
+// at n = 4..8 (5-11% slower: cfg2 0.208 vs 0.221 ms) nor the AoS pair kernel
+// (n=3..8: 2-12% slower) -- more registers where the kernel is HBM-bound.
+template <typename T, int n> constexpr bool kFastVec = sizeof(T) == 8;
+template <typename T, int n> constexpr bool kFastSoaPair = sizeof(T) == 8 && n >= 11;
+
 // SoA dense kernel, two adjacent points per thread (512-point tiles): x comes
 // in as one 16-byte load and every F_m row leaves as 16-byte streaming stores
 // (512 contiguous bytes per warp instruction, half the store instructions).
@@ -38,7 +47,7 @@ dense_soa_pair_kernel(const T* __restrict__ X, int64_t N, T* __restrict__ out,
     okb = okb || !in;
     T* o = out + i;
     T ta, tb;
-    eval_pair_stream<T, n>(
+    eval_pair_stream<T, n, kFastSoaPair<T, n>>(
         xv.x, xv.y, oka, okb, ta, tb,
         [&](int m, T a, T b) {
           V2 v;
@@ -152,7 +161,7 @@ dense_aos_vec_kernel(const T* __restrict__ X, int64_t N, T* __restrict__ out,
       if (in && !ok[j]) flag_domain(dom, index_base + i + j);
       ok[j] = ok[j] || !in;
     }
-    eval_multi_stream<T, n, P>(
+    eval_multi_stream<T, n, P, kFastVec<T, n>>(
         xv, ok, tv,
         [&](int m, const T (&v)[P]) {
 #pragma unroll

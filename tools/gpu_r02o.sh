@@ -1,0 +1,7 @@
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/ -q -m gpu -x > gpurun_out/pytest_o.log 2>&1
+echo "pytest rc=$?" >> gpurun_out/pytest_o.log; tail -n 2 gpurun_out/pytest_o.log
+timeout 800 python tools/order_sweep.py --out gpurun_out/r02_order_sweep.md > /dev/null 2>&1
+BOYS_LIB=$PWD/ab_libs/libboys_old.so timeout 800 python tools/order_sweep.py --out gpurun_out/sweep_old1.md > /dev/null 2>&1
+timeout 300 python tools/dense_rate.py
+echo done
