@@ -373,7 +373,7 @@ static boys_status launch_soa_pair(const T* x, int64_t N, T* out, T* expx, int64
   return launch_pdl(k, grid, 0, s, x, N, out, expx, dom, base);
 }
 
-// SoA, four adjacent points per thread (n <= 3: f64 2^24 n=0 113 vs 123 us,
+// SoA, four adjacent points per thread (n <= 5: f64 2^24 n=0 113 vs 123 us,
 // n=1 122 vs 135, n=3 152 vs 167; f32 n <= 2 9-13% faster), one block per
 // 1024-point tile (persistent: cfg1 10.8 vs 9.25 us), 4 resident blocks (59-64
 // registers; 3 / 2: slower), branch-free correctly rounded div/sqrt/rcp.
@@ -417,19 +417,23 @@ static boys_status launch_dense_t(const T* x, int64_t N, T* out, T* expx, int64_
                                   int64_t base, cudaStream_t s) {
   const bool al = aligned16(x) && aligned16(out) && (!expx || aligned16(expx));
   if constexpr (!AOS) {
-    if constexpr (n <= 3) {
+    // four points per thread (with the branch-free CR fast paths) up to n = 5:
+    // same-box sweep at 2^24, f64 n=4 0.1646 -> 0.1393 ms, n=5 0.1748 -> 0.1586
+    // vs the pair kernel; f32 n=4, 5 1-2% faster; slower from n = 6 (f64 n=7
+    // +20%: registers where the order is HBM-bound)
+    if constexpr (n <= 5) {
       if (N % 4 == 0 && al) return launch_soa_quad<T, n>(x, N, out, expx, dom, base, s);
     }
     if (N % 2 == 0 && al) return launch_soa_pair<T, n>(x, N, out, expx, dom, base, s);
     return launch_dense_k<T, n, false, 1, (n <= 1 ? 8 : 4)>(x, N, out, expx, dom, base, s);
   } else {
     if constexpr (n >= 1 && n <= 3) {
-      // register rows + direct 16-byte stores for n = 1, 2 and f32 n = 3 (2^24:
-      // n=1 f64 128.6 vs 158.2 us, f32 63.4 vs 91.2; n=2 f64 149.2 vs 168.1,
-      // f32 82.9 vs 96.2; f32 n=3 88.1 vs 97.8); the staged kernels win from
-      // f64 n = 3 (180 vs 173 us)
+      // register rows + direct 16-byte stores for n = 1..3 (2^24: n=1 f64 128.6
+      // vs 158.2 us, f32 63.4 vs 91.2; n=2 f64 149.2 vs 168.1, f32 82.9 vs
+      // 96.2; f32 n=3 88.1 vs 97.8; f64 n=3, with the CR fast paths, 0.1683 vs
+      // 0.1715 ms for the paired staged kernel; f64 n=4, 5 slower: +3%, +25%)
       constexpr int P = (n == 1 || (n == 2 && sizeof(T) == 8)) ? 4 : 2;
-      constexpr bool use = n <= 2 || sizeof(T) == 4;
+      constexpr bool use = true;
       if (use && N % P == 0 && al) return launch_aos_vec<T, n, P>(x, N, out, expx, dom, base, s);
     }
     // paired AoS where the double-buffered 512-point tile allows 3 blocks/SM

@@ -96,10 +96,11 @@ def test_config_inputs_bit_exact(oracle, cfg):
 
 @pytest.mark.parametrize("N", [0, 1, 2, 4, 255, 256, 257, 514, 1000, 1028, 2048, 65537, 65540])
 def test_sizes_and_tails(oracle, N):
-    # every dense kernel family: SoA quad (n <= 3, N % 4 == 0), SoA pair (N even),
-    # SoA one point (odd N), AoS register rows (n = 1, 2), AoS pair (n <= 8),
+    # every dense kernel family: SoA quad (n <= 5, N % 4 == 0), SoA pair (N even),
+    # SoA one point (odd N), AoS register rows (n = 1..3), AoS pair (n <= 8),
     # AoS one point (n >= 9); f32 for the f32-only defaults
-    for n, layout in ((16, "aos"), (12, "aos"), (8, "soa"), (3, "aos"), (0, "soa"), (1, "soa"),
+    for n, layout in ((16, "aos"), (15, "aos"), (12, "aos"), (8, "soa"), (3, "aos"), (4, "aos"),
+                      (0, "soa"), (1, "soa"), (4, "soa"), (5, "soa"),
                       (3, "soa"), (1, "aos"), (2, "aos"), (6, "aos")):
         x = np.abs(np.random.default_rng(N).standard_normal(N)) * 30
         got = boys(n, torch.from_numpy(x).cuda(), layout=layout).cpu().numpy()
