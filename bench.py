@@ -822,7 +822,7 @@ def hermite_line(ctx, steps, warmup, hbm_peak, fp64_peak, L=4, npairs=4096):
              "frac": round(gbs / hbm_peak, 4)} if bound == "hbm" else
             {"bound": "fp64", "achieved": round(tops / 1e12, 3), "peak": round(fp64_peak / 1e12, 3),
              "unit": "TDPop/s", "frac": round(tops / fp64_peak, 4)})
-    roof.update({"traffic": None, "algorithmic_bytes_per_launch": bytes_q * nq,
+    roof.update({"traffic": committed_traffic("hermite"), "algorithmic_bytes_per_launch": bytes_q * nq,
                  "bytes_per_quartet": bytes_q, "fp64_ops_per_quartet": ops,
                  "fp64_ops_frac": round(tops / fp64_peak, 4) if fp64_peak else None,
                  "launch_ms": round(ms, 4),

@@ -2,10 +2,10 @@
 # the report is summarised on the box (raw-page CSV + traffic json) and only the
 # headline cfg3 capture (with source) comes back, to stay under gpurun's 64 MiB.
 mkdir -p gpurun_out
-CF=cfg3,cfg2,cfg1,cfg4,cfg4f32,cfg5,split
+CF=cfg3,cfg2,cfg1,cfg4,cfg4f32,cfg5,split,hermite
 timeout 300 python tools/prof_kernels.py --configs $CF --launches 2 > gpurun_out/prof_plain.log 2>&1 && \
 timeout 1200 ncu --set full --clock-control none \
-    -k regex:"dense_kernel|dense_soa_pair|dense_soa_quad|ragged_kernel|split_kernel" -c 14 \
+    -k regex:"dense_kernel|dense_soa_pair|dense_soa_quad|ragged_kernel|split_kernel|hermite_kernel" -c 16 \
     -o /tmp/prof_r02 python tools/prof_kernels.py --configs $CF --launches 2 > gpurun_out/ncu_full.log 2>&1
 echo "ncu full rc=$?"
 ncu -i /tmp/prof_r02.ncu-rep --page raw --csv > gpurun_out/prof_r02_raw.csv 2>&1

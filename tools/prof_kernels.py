@@ -15,6 +15,14 @@ ap.add_argument("--launches", type=int, default=3)
 a = ap.parse_args()
 dev = torch.device("cuda:0")
 for name in a.configs.split(","):
+    if name == "hermite":                    # fused consumer, 4096^2 quartets at L = 4
+        from paper_2504_07637_b200 import hermite_coulomb
+        b, k = W.shell_pairs(4096, seed=21, device=dev), W.shell_pairs(4096, seed=22, device=dev)
+        for _ in range(a.launches):
+            hermite_coulomb(4, b, k, check=False)
+        torch.cuda.synchronize()
+        print(name, "ok", flush=True)
+        continue
     if name == "split":                      # eval_with_split(16, 8) on the cfg3 inputs, AoS
         x = W.config_x("cfg3", device=dev)
         out = torch.empty((x.numel(), 17), dtype=torch.float64, device=dev)
