@@ -985,7 +985,8 @@ def main():
 
     # the other BASELINE configurations (same protocol, fewer steps)
     extras_list = (args.extras.split(",") if args.extras else
-                   (["cfg1", "cfg1_l2flush", "cfg2", "cfg4", "cfg4f32", "cfg5", "split", "hermite"]
+                   (["cfg1", "cfg1_l2flush", "cfg1_2p24", "cfg2", "cfg4", "cfg4f32", "cfg5", "split",
+                     "hermite"]
                     if ctx.ws == 1 else ["cfg5"]))
     if not args.no_extras:
         extras = {}
@@ -1003,7 +1004,10 @@ def main():
         # alternating, so dirty L2 lines of one launch are written back during
         # the next instead of being overwritten in L2 (which would flatter HBM)
         plan = {"cfg1": ("cfg1", 32, "graph"), "cfg1_l2flush": ("cfg1", 1, "flush"),
-                "cfg2": ("cfg2", 2, None)}
+                "cfg2": ("cfg2", 2, None),
+                # the n=0 kernel at steady state: cfg1's distribution, 2^24-point
+                # batches (27 waves: no per-launch ramp/tail), two alternating
+                "cfg1_2p24": ("cfg1", 2, None, 1 << 24)}
         for key in extras_list:
             if key == "hermite":
                 try:
@@ -1012,11 +1016,11 @@ def main():
                 except Exception as ex:  # noqa: BLE001
                     extras[key] = {"error": str(ex)[:300]}
                 continue
-            name, rot, fl = plan.get(key, (key, 1, None))
+            name, rot, fl, npts = (plan.get(key, (key, 1, None)) + (None,))[:4]
             if name == args.config:
                 continue
             try:
-                w2 = make_workload(name, ctx, rotate=rot)
+                w2 = make_workload(name, ctx, n_points=npts, rotate=rot)
                 k = min(args.steps, 50) if name != "cfg1" else (100 if rot > 1 else 200)
                 r2 = time_workload(w2, ctx, k, args.warmup,
                                    flush=(lambda: flushbuf.zero_()) if fl == "flush" else None,
@@ -1029,6 +1033,10 @@ def main():
                             "CUDA-graph replay "
                             f"({rot} x {w2.bytes_per_point * w2.points_per_step / rot / 2**20:.0f} MiB "
                             "working set > L2)")
+                elif key == "cfg1_2p24":
+                    note = ("cfg1's distribution at 2^24 points per batch (not the config's "
+                            "2^20): the kernel without per-launch ramp and tail; "
+                            f"{rot} alternating batches with their own outputs (> L2)")
                 elif rot > 1:
                     note = (f"{rot} distinct batches per step with their own outputs "
                             f"({w2.bytes_per_point * w2.points_per_step / rot / 2**30:.2f} GiB per "
