@@ -105,6 +105,38 @@ template <> struct Sentinel<float> {
   static __device__ __forceinline__ bool is(float v) { return __float_as_int(v) == 0x7fa0c0de; }
 };
 
+// high word of the bit pattern (fp64) / the bit pattern (fp32)
+__device__ __forceinline__ unsigned hi_word(double v) { return (unsigned)__double2hiint(v); }
+__device__ __forceinline__ unsigned hi_word(float v) { return __float_as_uint(v); }
+
+// Chunk-path test on x, one integer compare: fp64 -- positive, finite and
+// below `bound_hi` (the high word of the smallest staged x_up, a power of
+// two), so the upward ladder is not needed; fp32 -- positive and finite
+// (x > x_up joins the queue there).  -0.0 fails it and takes the general path.
+template <typename T>
+__device__ __forceinline__ bool hot_x(T x, unsigned bound_hi) {
+  return hi_word(x) < (sizeof(T) == 8 ? bound_hi : 0x7f800000u);
+}
+
+// General per-element path (kept out of line: it is cold and large): element
+// `idx` evaluated from the __constant__ rows at any tabulated order and
+// written directly at its offset; NaN row and domain flag for invalid x or an
+// order above the table.
+template <typename T>
+__device__ __noinline__ void ragged_general_element(T x, int n, int64_t goff, bool in, int64_t idx,
+                                                    T* __restrict__ out, int64_t* __restrict__ dom) {
+  constexpr int MAXN = Tab<T>::MAX_ORDER;
+  const bool okl = in && valid_x(x) && n <= MAXN;
+  if (in && !okl) {
+    flag_domain(dom, idx);
+    for (int m = 0; m <= n; ++m) out[goff + m] = Ar<T>::nan();
+  }
+  T* dst = out + goff;
+  eval_point_rt<T, MAXN>(x, okl, okl ? n : 0, ConstRows<T>{}, [&](int m, T v) {
+    if (okl) dst[m] = v;
+  });
+}
+
 template <typename T, int NB, int EPL, int CPE, int MINB, int WT = kThreads>
 __global__ void __launch_bounds__(WT, MINB)
 ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
@@ -163,52 +195,46 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
       plast_off = __ldg(OFF + ((j0 + CH < N) ? j0 + CH : N));
     }
   };
+  // hot-path bound on x: below every staged order's x_up (fp64: the upward
+  // ladder then never runs in the chunk path; such x take the general path)
+  unsigned xup_hi_min = 0x7ff00000u;
+  if (!kDeferUp<T>) {
+    for (int k = 0; k <= NB; ++k) xup_hi_min = min(xup_hi_min, hi_word(Tab<T>::row(k).x_up));
+  }
+  const unsigned lt_mask = (1u << lane) - 1u;
   load(c);
   for (; c < nchunks; c += wstride) {
     const int64_t i0 = c * CH;
     T x[EPL];
     int n[EPL];
     int64_t goff[EPL];
-    bool in[EPL];
     const int rem = prem;
 #pragma unroll
     for (int e = 0; e < EPL; ++e) {
       x[e] = px[e];
       n[e] = pn[e];
       goff[e] = poff[e];
-      in[e] = 32 * e + lane < rem;
     }
     const int64_t base = pbase, cnt = plast_off - pbase;
     load(c + wstride);
-    constexpr int MAXN = Tab<T>::MAX_ORDER;
-    bool xok[EPL], slow = cnt > WarpT::CAP;
+    // The chunk path below assumes a full chunk of valid elements (x finite,
+    // >= 0 and, in fp64, below x_up; order <= NB) whose offsets are the prefix
+    // sum of n + 1 and whose output range fits the staging slot.  Anything else
+    // -- the batch's last partial chunk, invalid x or orders, gapped offsets,
+    // orders above the fast path's bound -- takes the general per-element path.
+    bool slow = rem != CH || cnt > WarpT::CAP;
     int cnt_l = 0;
 #pragma unroll
     for (int e = 0; e < EPL; ++e) {
-      xok[e] = valid_x(x[e]);
-      if (in[e] && !(xok[e] && n[e] <= MAXN)) flag_domain(dom, i0 + 32 * e + lane);
-      slow = slow || (in[e] && n[e] > NB);
-      cnt_l += in[e] ? n[e] + 1 : 0;
+      slow = slow || !hot_x<T>(x[e], xup_hi_min) || n[e] > NB;
+      cnt_l += n[e] + 1;
     }
-    // offsets that are not the chunk's prefix sum (gaps between elements):
-    // the staged range would not match, so write per element at offsets[i]
     const int64_t cnt_sum = (int64_t)__reduce_add_sync(kFull, (unsigned)cnt_l);   // every lane
     slow = slow || cnt_sum != cnt;
     if (__any_sync(kFull, slow)) {
-      // an order above the fast path's bound (or an output range above the
-      // staging capacity): every lane evaluates its own elements from the
-      // __constant__ rows and writes them directly (NaN above the table)
 #pragma unroll
-      for (int e = 0; e < EPL; ++e) {
-        const bool okl = in[e] && xok[e] && n[e] <= MAXN;
-        if (in[e] && !okl) {                       // NaN row (domain flagged above)
-          for (int m = 0; m <= n[e]; ++m) out[goff[e] + m] = A::nan();
-        }
-        T* dst = out + goff[e];
-        eval_point_rt<T, MAXN>(x[e], okl, okl ? n[e] : 0, ConstRows<T>{}, [&](int m, T v) {
-          if (okl) dst[m] = v;
-        });
-      }
+      for (int e = 0; e < EPL; ++e)
+        ragged_general_element<T>(x[e], n[e], goff[e], 32 * e + lane < rem, i0 + 32 * e + lane, out, dom);
       continue;
     }
     // staging position matches the global 16-byte phase of the chunk range
@@ -218,57 +244,96 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
     // the previous chunk's bulk store must have finished reading the slot
     if (lane == 0) bulk_wait_read<0>();
     __syncwarp();
-    T xs[EPL], t[EPL], cur[EPL], tx[EPL];
+    T t[EPL], cur[EPL], tx[EPL];
     ZcRow<T> zc[EPL];
     T* dst[EPL];
     bool wr[EPL];
     int wmax_l = 0;
+    // The math below is written phase by phase over all EPL elements with no
+    // branch between the elements of a phase, so each phase is one basic block
+    // and the elements' independent dependency chains interleave (FP64: 8-cycle
+    // DFMA latency; element-by-element code left the warp waiting on one chain).
     // (evaluating e^{-x} only for the elements with x <= XEXP, compacted one
     // per lane, measured no faster: tools/ab/ab24.sh)
 #pragma unroll
+    for (int e = 0; e < EPL; ++e) zc[e] = S.zc[n[e]];
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) t[e] = exp_neg_select(x[e]);
+#pragma unroll
     for (int e = 0; e < EPL; ++e) {
-      const bool ok = in[e] && xok[e];
-      xs[e] = ok ? x[e] : A::nan();                // NaN propagates through the tail
-      const T xe = ok ? x[e] : T(0);
-      t[e] = exp_neg_select(xe);
-      zc[e] = S.zc[n[e]];
       // deferred to the warp queue: below the cut-off (Q~ needed) and, in
-      // fp32, above x_up (upward ladder)
-      const bool defer = ok && (xe < zc[e].z || (kDeferUp<T> && xe > zc[e].x_up));
+      // fp32, above x_up (upward ladder).  Branch-free enqueue; qn stays
+      // warp-uniform.
+      const bool defer = x[e] < zc[e].z || (kDeferUp<T> && x[e] > zc[e].x_up);
       const unsigned dmask = __ballot_sync(kFull, defer);
       dst[e] = W.stage + (int)(goff[e] - base) + shift;
-      if (dmask) {                                 // enqueue (qn stays warp-uniform)
-        if (defer) {
-          const int slot = qn + __popc(dmask & ((1u << lane) - 1u));
-          W.qx[slot] = xe;
-          W.qt[slot] = t[e];
-          W.qn[slot] = (unsigned char)n[e];
-          W.qoff[slot] = goff[e];
-        }
-        qn += __popc(dmask);
+      const int slot = qn + __popc(dmask & lt_mask);
+      if (defer) {
+        W.qx[slot] = x[e];
+        W.qt[slot] = t[e];
+        W.qn[slot] = (unsigned char)n[e];
+        W.qoff[slot] = goff[e];
       }
-      wr[e] = in[e] && !defer;
-      wmax_l = max(wmax_l, wr[e] ? n[e] : 0);
+      qn += __popc(dmask);
+      wr[e] = !defer;
+      wmax_l = max(wmax_l, defer ? 0 : n[e]);
     }
     // immediate elements (past the cut-off): y = x.  Same operation sequence
     // as seed<T, n> + the recursion (+ the upward ladder in fp64).
     {
       const int wmax = __reduce_max_sync(kFull, (unsigned)wmax_l);
       const int bits = 32 - __clz(wmax | 1);
-      T r[EPL], sr[EPL];
+      T r[EPL], sr[EPL], xr[EPL];
+      // correctly rounded 1/x and sqrt through their branch-free fast paths
+      // (bit-identical to the intrinsics); deferred elements get a harmless
+      // operand so x = 0 in the queue does not send the warp to the intrinsic
+      bool slow = false;
 #pragma unroll
       for (int e = 0; e < EPL; ++e) {
-        r[e] = A::rcp(xs[e]);
-        sr[e] = A::sqrt(r[e]);
+        xr[e] = wr[e] ? x[e] : T(1);
+        bool sj;
+        r[e] = A::rcp_fast(xr[e], sj);
+        slow = slow || sj;
+      }
+      if (__any_sync(kFull, slow)) {
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) r[e] = A::rcp(xr[e]);
+      }
+      slow = false;
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) {
+        bool sj;
+        sr[e] = A::sqrt_fast(r[e], sj);
+        slow = slow || sj;
+      }
+      if (__any_sync(kFull, slow)) {
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) sr[e] = A::sqrt(r[e]);
+      }
+      // r^n, bit by bit over all elements (powi_rt_bounded's product sequence)
+      T pw[EPL], pp[EPL];
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) {
+        pw[e] = (n[e] & 1) ? r[e] : T(1);
+        pp[e] = r[e];
+      }
+#pragma unroll
+      for (int j = 1; j < 5; ++j) {
+        if (j >= bits) break;
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) pp[e] = A::mul(pp[e], pp[e]);
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) pw[e] = A::mul(pw[e], ((n[e] >> j) & 1) ? pp[e] : T(1));
       }
 #pragma unroll
       for (int e = 0; e < EPL; ++e) {
-        const T cn = zc[e].c;
-        // n = 0: powi gives exactly 1.0 and (c * 1.0) * sr == c * sr, so no select
-        cur[e] = A::mul(A::mul(cn, powi_rt_bounded(r[e], n[e], bits)), sr[e]);
+        // n = 0: the power is exactly 1.0 and (c * 1.0) * sr == c * sr, so no select
+        cur[e] = A::mul(A::mul(zc[e].c, pw[e]), sr[e]);
+        tx[e] = A::add(x[e], x[e]);
+      }
+#pragma unroll
+      for (int e = 0; e < EPL; ++e)
         if (wr[e]) dst[e][n[e]] = cur[e];
-        tx[e] = A::add(xs[e], xs[e]);
-      }
       // recursion steps m = wmax-1 .. 0: enter the unrolled chain once through
       // a jump table (wmax is warp-uniform) instead of testing every step
       // one predicate per element and step: elements that are not written
@@ -278,12 +343,15 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
       for (int e = 0; e < EPL; ++e) neff[e] = wr[e] ? n[e] : 0;
 #define BOYS_STEP(M)                                                       \
   if ((M) < NB) {                                                           \
-    _Pragma("unroll") for (int e = 0; e < EPL; ++e) {                       \
-      const T nx = A::mul(A::fma(tx[e], cur[e], t[e]), rinv<T>((M) < NB ? (M) : 0)); \
-      const bool on = (M) < neff[e];                                        \
-      pmov(on, cur[e], nx);                                                 \
-      psts(on, dst[e] + (M), cur[e]);                                       \
-    }                                                                       \
+    T nx[EPL];                                                              \
+    _Pragma("unroll") for (int e = 0; e < EPL; ++e)                         \
+      nx[e] = A::fma(tx[e], cur[e], t[e]);                                  \
+    _Pragma("unroll") for (int e = 0; e < EPL; ++e)                         \
+      nx[e] = A::mul(nx[e], rinv<T>((M) < NB ? (M) : 0));                   \
+    _Pragma("unroll") for (int e = 0; e < EPL; ++e)                         \
+      pmov((M) < neff[e], cur[e], nx[e]);                                   \
+    _Pragma("unroll") for (int e = 0; e < EPL; ++e)                         \
+      psts((M) < neff[e], dst[e] + (M), cur[e]);                            \
   }
       switch (wmax) {
         case 16: BOYS_STEP(15) [[fallthrough]];
@@ -306,28 +374,6 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
       }
 #undef BOYS_STEP
       static_assert(NB <= 16, "extend the recursion jump table");
-      if (!kDeferUp<T>) {
-        bool up[EPL], anyup = false;
-#pragma unroll
-        for (int e = 0; e < EPL; ++e) {
-          up[e] = wr[e] && xs[e] > zc[e].x_up;   // NaN (invalid) compares false
-          anyup = anyup || up[e];
-        }
-        if (__any_sync(kFull, anyup)) {
-#pragma unroll
-          for (int e = 0; e < EPL; ++e) {
-            const T rx = A::rcp(xs[e]);
-            T f = up_first(xs[e]);
-            if (up[e]) dst[e][0] = f;
-#pragma unroll
-            for (int m = 0; m < NB; ++m) {
-              if (m >= wmax) break;
-              f = up_next(f, m, rx);
-              if (up[e] && m + 1 <= n[e]) dst[e][m + 1] = f;
-            }
-          }
-        }
-      }
     }
     __syncwarp();
     // the chunk's output range [base, base + cnt): scalar head/tail to reach
@@ -598,8 +644,22 @@ static boys_status launch_ragged(const void* x, const uint8_t* nm, const int64_t
     // 12 staged values per element (8: 1.96 ms f64; 2 elements x 10 values,
     // 24 warps/SM: within 1% but overflows to the slow path from order 10;
     // 128-thread blocks / 96-register bound: f64 1.84-2.36 vs 1.78 ms)
-    constexpr int EPL = sizeof(T) == 8 ? 3 : 4, CPE = 12;
-    boys_status st = launch_chunks<T, NB, EPL, CPE, 0>(x, nm, off, N, out, dom, s);
+#ifndef BOYS_AB_EPL64
+#define BOYS_AB_EPL64 3
+#endif
+#ifndef BOYS_AB_EPL32
+#define BOYS_AB_EPL32 4
+#endif
+#ifndef BOYS_AB_CPE
+#define BOYS_AB_CPE 12
+#endif
+    constexpr int EPL = sizeof(T) == 8 ? BOYS_AB_EPL64 : BOYS_AB_EPL32, CPE = BOYS_AB_CPE;
+    // fp32: three resident blocks (80 registers)
+#ifndef BOYS_AB_F32_MINB
+#define BOYS_AB_F32_MINB 0
+#endif
+    constexpr int MINB = sizeof(T) == 8 ? 0 : BOYS_AB_F32_MINB;
+    boys_status st = launch_chunks<T, NB, EPL, CPE, MINB>(x, nm, off, N, out, dom, s);
     if (st != BOYS_OK) return st;
   }
   g_launches.fetch_add(1, std::memory_order_relaxed);
