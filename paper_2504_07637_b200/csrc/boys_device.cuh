@@ -184,7 +184,7 @@ __device__ __forceinline__ void seed_multi_fast(const double (&x)[P], const doub
     }
     if (__any_sync(kFull, slow)) {
 #pragma unroll
-      for (int j = 0; j < P; ++j) sq[j] = A::sqrt(Q[j]);
+      for (int j = 0; j < P; ++j) sq[j] = A::sqrt_cold(Q[j]);
     }
 #pragma unroll
     for (int j = 0; j < P; ++j) {
@@ -203,7 +203,7 @@ __device__ __forceinline__ void seed_multi_fast(const double (&x)[P], const doub
   }
   if (__any_sync(kFull, slow)) {
 #pragma unroll
-    for (int j = 0; j < P; ++j) r[j] = A::rcp(y[j]);
+    for (int j = 0; j < P; ++j) r[j] = A::rcp_cold(y[j]);
   }
   slow = false;
 #pragma unroll
@@ -214,7 +214,7 @@ __device__ __forceinline__ void seed_multi_fast(const double (&x)[P], const doub
   }
   if (__any_sync(kFull, slow)) {
 #pragma unroll
-    for (int j = 0; j < P; ++j) sr[j] = A::sqrt(r[j]);
+    for (int j = 0; j < P; ++j) sr[j] = A::sqrt_cold(r[j]);
   }
 #pragma unroll
   for (int j = 0; j < P; ++j)

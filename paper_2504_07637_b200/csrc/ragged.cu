@@ -297,7 +297,7 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
       }
       if (__any_sync(kFull, slow)) {
 #pragma unroll
-        for (int e = 0; e < EPL; ++e) r[e] = A::rcp(xr[e]);
+        for (int e = 0; e < EPL; ++e) r[e] = A::rcp_cold(xr[e]);
       }
       slow = false;
 #pragma unroll
@@ -308,7 +308,7 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
       }
       if (__any_sync(kFull, slow)) {
 #pragma unroll
-        for (int e = 0; e < EPL; ++e) sr[e] = A::sqrt(r[e]);
+        for (int e = 0; e < EPL; ++e) sr[e] = A::sqrt_cold(r[e]);
       }
       // r^n, bit by bit over all elements (powi_rt_bounded's product sequence)
       T pw[EPL], pp[EPL];
@@ -658,7 +658,10 @@ static boys_status launch_ragged(const void* x, const uint8_t* nm, const int64_t
 #ifndef BOYS_AB_F32_MINB
 #define BOYS_AB_F32_MINB 0
 #endif
-    constexpr int MINB = sizeof(T) == 8 ? 0 : BOYS_AB_F32_MINB;
+#ifndef BOYS_AB_F64_MINB
+#define BOYS_AB_F64_MINB 0
+#endif
+    constexpr int MINB = sizeof(T) == 8 ? BOYS_AB_F64_MINB : BOYS_AB_F32_MINB;
     boys_status st = launch_chunks<T, NB, EPL, CPE, MINB>(x, nm, off, N, out, dom, s);
     if (st != BOYS_OK) return st;
   }
