@@ -32,6 +32,13 @@ __device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, uint32_
                : "memory");
   asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
 }
+// the same with raw operands (global address, shared address, bytes)
+__device__ __forceinline__ void bulk_store_u(uint64_t gdst, uint32_t ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(gdst),
+               "r"(ssrc), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+}
 template <int PENDING>
 __device__ __forceinline__ void bulk_wait_read() {
   asm volatile("cp.async.bulk.wait_group.read %0;\n" ::"n"(PENDING) : "memory");
@@ -66,6 +73,10 @@ __device__ __forceinline__ void pmov(bool p, float& dst, float v) {
 __device__ __forceinline__ void psts(bool p, double* a, double v) {
   asm volatile("{ .reg .pred q; setp.ne.b32 q, %2, 0; @q st.shared.f64 [%0], %1; }"
                :: "r"(smem_u32(a)), "d"(v), "r"((int)p) : "memory");
+}
+__device__ __forceinline__ void psts(bool p, int64_t* a, int64_t v) {
+  asm volatile("{ .reg .pred q; setp.ne.b32 q, %2, 0; @q st.shared.b64 [%0], %1; }"
+               :: "r"(smem_u32(a)), "l"(v), "r"((int)p) : "memory");
 }
 __device__ __forceinline__ void psts(bool p, float* a, float v) {
   asm volatile("{ .reg .pred q; setp.ne.b32 q, %2, 0; @q st.shared.f32 [%0], %1; }"

@@ -35,9 +35,10 @@ struct RaggedWarp {
   static constexpr int CAP = 32 * EPL * (CPE < NB + 1 ? CPE : NB + 1);
   static constexpr int QCAP = 32 * EPL + 32;      // < 32 left after a drain + one chunk
   alignas(16) T stage[CAP + 16 / sizeof(T)];
-  T qx[QCAP], qt[QCAP];
-  int64_t qoff[QCAP];
-  unsigned char qn[QCAP];
+  // deferred elements, by index: the drain reloads x, order and offset (cache
+  // hits: the chunk pass has just read them) and recomputes e^{-x}.  One store
+  // per element slot in the chunk pass instead of four (x, t, order, offset).
+  int64_t qidx[QCAP];
   T scratch[32];
 };
 
@@ -57,21 +58,25 @@ struct RaggedSmem {
 template <typename T> constexpr bool kDeferUp = sizeof(T) == 4;
 
 // Evaluate up to 32 queued elements (one per lane), writing straight to
-// global memory.
+// global memory; returns the new queue length.  Out of line: it runs once per
+// ~7 chunks of an ERI-like batch, and inlined into the chunk loop its
+// constants (22 uniform loads) and registers were paid on every chunk.
 template <typename T, int NB, typename WarpT>
-__device__ __forceinline__ void ragged_drain(WarpT& W, const SmemRows<T>& st,
-                                             int& qn, int lane, T* __restrict__ out) {
+__device__ __noinline__ int ragged_drain(WarpT& W, SmemRows<T> st, int qn, const T* __restrict__ X,
+                                         const uint8_t* __restrict__ NM,
+                                         const int64_t* __restrict__ OFF, T* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
   // queued elements' slots were written (with stale staging data) by earlier
   // bulk stores of their chunks: those must be complete before we overwrite
   if (lane == 0) bulk_wait_all();
   __syncwarp();
   const int take = qn < 32 ? qn : 32;
   const bool has = lane < take;
-  const int slot = qn - take + lane;            // LIFO: drain the newest `take` entries
-  const T x = has ? W.qx[slot] : T(0);
-  const T t = has ? W.qt[slot] : T(0);
-  const int n = has ? (int)W.qn[slot] : 0;
-  const int64_t off = has ? W.qoff[slot] : 0;
+  const int64_t idx = has ? W.qidx[qn - take + lane] : 0;   // LIFO: the newest `take` entries
+  const T x = has ? ldg_nc(X + idx) : T(0);
+  const int n = has ? (int)NM[idx] : 0;
+  const int64_t off = has ? __ldg(OFF + idx) : 0;
+  const T t = exp_neg_select(x);
   __syncwarp();
   // queued: below the cut-off (Q~ branch) or above x_up (asymptotic branch,
   // values from the upward ladder inside tail_rt)
@@ -90,20 +95,8 @@ __device__ __forceinline__ void ragged_drain(WarpT& W, const SmemRows<T>& st,
   T* sink = W.scratch + lane;
   tail_rt<T, NB>(x, y, t, n, has, wmax, st,
                  [&](int m, T v, bool on) { *((has && on) ? dst + m : sink) = v; });
-  qn -= take;
+  return qn - take;
 }
-
-// Staging sentinel for deferred elements' slots: a NaN payload the arithmetic
-// never produces (IEEE ops return the canonical quiet NaN).
-template <typename T> struct Sentinel;
-template <> struct Sentinel<double> {
-  static __device__ __forceinline__ double value() { return __longlong_as_double(0x7ff4c0de5e47e1e1LL); }
-  static __device__ __forceinline__ bool is(double v) { return __double_as_longlong(v) == 0x7ff4c0de5e47e1e1LL; }
-};
-template <> struct Sentinel<float> {
-  static __device__ __forceinline__ float value() { return __int_as_float(0x7fa0c0de); }
-  static __device__ __forceinline__ bool is(float v) { return __float_as_int(v) == 0x7fa0c0de; }
-};
 
 // high word of the bit pattern (fp64) / the bit pattern (fp32)
 __device__ __forceinline__ unsigned hi_word(double v) { return (unsigned)__double2hiint(v); }
@@ -155,44 +148,51 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
   const SmemRows<T> rows{S.st.row};
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   WarpT& W = S.w[wid];
-  const int64_t nchunks = (N + CH - 1) / CH;
+  const int64_t nfull = N / CH;                  // full chunks: the loop below
   const int64_t wstride = (int64_t)gridDim.x * (WT / 32);
   int qn = 0;                                    // warp-uniform queue length
   int64_t c = (int64_t)blockIdx.x * (WT / 32) + wid;
-  // software pipeline: inputs of chunk c are loaded one iteration ahead
-  T px[EPL];
-  int pn[EPL];
-  int64_t poff[EPL], pbase = 0, plast_off = 0;
-  int prem = 0;                                  // elements of the prefetched chunk
-  auto load = [&](int64_t cc) {
-    const int64_t j0 = cc * CH;
-    if (j0 + CH <= N) {                          // full chunk (warp-uniform): no predicates
-      prem = CH;
-      const T* xp = X + j0 + lane;
-      const uint8_t* np = NM + j0 + lane;
-      const int64_t* op = OFF + j0 + lane;
+  // software pipeline: inputs of the warp's next chunk are loaded one
+  // iteration ahead through running pointers (lane's first element of it)
+  const T* xp = X + c * CH + lane;
+  const uint8_t* np = NM + c * CH + lane;
+  const int64_t* op = OFF + c * CH + lane;
+  const int64_t pstep = wstride * CH;
+  // Prefetch of the warp's next chunk, two ways (same-box A/B, cfg4):
+  //  * fp64 (kTwoSets): a second register set loaded at the top of the
+  //    iteration, a whole iteration ahead, and copied at the next top.  With 16
+  //    warps per SM the shorter distance below left long-scoreboard stalls at
+  //    the loop top (1.53-1.60 vs 1.50 ms) although it issues 8% fewer
+  //    instructions.
+  //  * fp32: x / n / goff themselves are reloaded in the middle of the
+  //    iteration, right after their last use (before the recursion steps): no
+  //    second set, no copies, 70 registers, so three blocks per SM hide the
+  //    shorter distance (0.775 vs 0.873 ms; loading earlier, after the enqueue,
+  //    needs 83 registers: 0.81-0.86 ms).
+  constexpr bool kTwoSets = sizeof(T) == 8;
+  T x[EPL], px[EPL];
+  int n[EPL], pn[EPL];
+  int64_t goff[EPL], poff[EPL], last_off = 0, plast_off = 0;
+  auto load = [&](T (&lx)[EPL], int (&ln)[EPL], int64_t (&lo)[EPL], int64_t& llast) {
 #pragma unroll
-      for (int e = 0; e < EPL; ++e) {
-        px[e] = ldg_nc(xp + 32 * e);
-        pn[e] = (int)np[32 * e];
-        poff[e] = __ldg(op + 32 * e);
-      }
-    } else {
-      // elements of chunk cc that exist (warp-uniform, 0 past the end)
-      const int rem = cc < nchunks ? (int)(N - j0) : 0;
-      prem = rem;
-#pragma unroll
-      for (int e = 0; e < EPL; ++e) {
-        const int64_t j = j0 + 32 * e + lane;
-        const bool jin = 32 * e + lane < rem;
-        px[e] = jin ? ldg_nc(X + j) : T(0);
-        pn[e] = jin ? (int)NM[j] : 0;
-        poff[e] = jin ? __ldg(OFF + j) : 0;
-      }
+    for (int e = 0; e < EPL; ++e) {
+      lx[e] = ldg_nc(xp + 32 * e);
+      ln[e] = (int)np[32 * e];
+      lo[e] = __ldg(op + 32 * e);
     }
-    if (cc < nchunks) {
-      pbase = __ldg(OFF + j0);
-      plast_off = __ldg(OFF + ((j0 + CH < N) ? j0 + CH : N));
+    llast = __ldg(op + (CH - lane));             // OFF[first + CH]: the range's end
+  };
+  // next chunk of this warp: advance, and load its inputs if it is a full one
+  bool have;
+  auto advance = [&]() {
+    c += wstride;
+    xp += pstep;
+    np += pstep;
+    op += pstep;
+    have = c < nfull;
+    if (have) {
+      if (kTwoSets) load(px, pn, poff, plast_off);
+      else load(x, n, goff, last_off);
     }
   };
   // hot-path bound on x: below every staged order's x_up (fp64: the upward
@@ -202,27 +202,31 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
     for (int k = 0; k <= NB; ++k) xup_hi_min = min(xup_hi_min, hi_word(Tab<T>::row(k).x_up));
   }
   const unsigned lt_mask = (1u << lane) - 1u;
-  load(c);
-  for (; c < nchunks; c += wstride) {
-    const int64_t i0 = c * CH;
-    T x[EPL];
-    int n[EPL];
-    int64_t goff[EPL];
-    const int rem = prem;
+  have = c < nfull;
+  if (have) {
+    if (kTwoSets) load(px, pn, poff, plast_off);
+    else load(x, n, goff, last_off);
+  }
+  while (have) {
+    const int64_t il = c * CH + lane;            // the lane's first element
+    if (kTwoSets) {
 #pragma unroll
-    for (int e = 0; e < EPL; ++e) {
-      x[e] = px[e];
-      n[e] = pn[e];
-      goff[e] = poff[e];
+      for (int e = 0; e < EPL; ++e) {
+        x[e] = px[e];
+        n[e] = pn[e];
+        goff[e] = poff[e];
+      }
+      last_off = plast_off;
+      advance();
     }
-    const int64_t base = pbase, cnt = plast_off - pbase;
-    load(c + wstride);
+    // the range's start OFF[c * CH] is lane 0's first offset
+    const int64_t base = __shfl_sync(kFull, goff[0], 0), cnt = last_off - base;
     // The chunk path below assumes a full chunk of valid elements (x finite,
     // >= 0 and, in fp64, below x_up; order <= NB) whose offsets are the prefix
     // sum of n + 1 and whose output range fits the staging slot.  Anything else
-    // -- the batch's last partial chunk, invalid x or orders, gapped offsets,
+    // -- invalid x or orders, gapped offsets,
     // orders above the fast path's bound -- takes the general per-element path.
-    bool slow = rem != CH || cnt > WarpT::CAP;
+    bool slow = cnt > WarpT::CAP;
     int cnt_l = 0;
 #pragma unroll
     for (int e = 0; e < EPL; ++e) {
@@ -234,7 +238,8 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
     if (__any_sync(kFull, slow)) {
 #pragma unroll
       for (int e = 0; e < EPL; ++e)
-        ragged_general_element<T>(x[e], n[e], goff[e], 32 * e + lane < rem, i0 + 32 * e + lane, out, dom);
+        ragged_general_element<T>(x[e], n[e], goff[e], true, il + 32 * e, out, dom);
+      if (!kTwoSets) advance();
       continue;
     }
     // staging position matches the global 16-byte phase of the chunk range
@@ -268,12 +273,7 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
       const unsigned dmask = __ballot_sync(kFull, defer);
       dst[e] = W.stage + (int)(goff[e] - base) + shift;
       const int slot = qn + __popc(dmask & lt_mask);
-      if (defer) {
-        W.qx[slot] = x[e];
-        W.qt[slot] = t[e];
-        W.qn[slot] = (unsigned char)n[e];
-        W.qoff[slot] = goff[e];
-      }
+      psts(defer, &W.qidx[slot], il + 32 * e);
       qn += __popc(dmask);
       wr[e] = !defer;
       wmax_l = max(wmax_l, defer ? 0 : n[e]);
@@ -284,13 +284,21 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
       const int wmax = __reduce_max_sync(kFull, (unsigned)wmax_l);
       const int bits = 32 - __clz(wmax | 1);
       T r[EPL], sr[EPL], xr[EPL];
-      // correctly rounded 1/x and sqrt through their branch-free fast paths
-      // (bit-identical to the intrinsics); deferred elements get a harmless
-      // operand so x = 0 in the queue does not send the warp to the intrinsic
-      bool slow = false;
+      // everything still needed of x and n (deferred elements: a harmless 1/x
+      // operand, so x = 0 in the queue does not send the warp to the cold
+      // path, and order 0: no recursion steps, their values are never used)
+      int neff[EPL];
 #pragma unroll
       for (int e = 0; e < EPL; ++e) {
         xr[e] = wr[e] ? x[e] : T(1);
+        tx[e] = A::add(x[e], x[e]);
+        neff[e] = wr[e] ? n[e] : 0;
+      }
+      // correctly rounded 1/x and sqrt through their branch-free fast paths
+      // (bit-identical to the intrinsics)
+      bool slow = false;
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) {
         bool sj;
         r[e] = A::rcp_fast(xr[e], sj);
         slow = slow || sj;
@@ -314,7 +322,7 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
       T pw[EPL], pp[EPL];
 #pragma unroll
       for (int e = 0; e < EPL; ++e) {
-        pw[e] = (n[e] & 1) ? r[e] : T(1);
+        pw[e] = (neff[e] & 1) ? r[e] : T(1);
         pp[e] = r[e];
       }
 #pragma unroll
@@ -323,24 +331,21 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
 #pragma unroll
         for (int e = 0; e < EPL; ++e) pp[e] = A::mul(pp[e], pp[e]);
 #pragma unroll
-        for (int e = 0; e < EPL; ++e) pw[e] = A::mul(pw[e], ((n[e] >> j) & 1) ? pp[e] : T(1));
+        for (int e = 0; e < EPL; ++e) pw[e] = A::mul(pw[e], ((neff[e] >> j) & 1) ? pp[e] : T(1));
       }
 #pragma unroll
       for (int e = 0; e < EPL; ++e) {
         // n = 0: the power is exactly 1.0 and (c * 1.0) * sr == c * sr, so no select
         cur[e] = A::mul(A::mul(zc[e].c, pw[e]), sr[e]);
-        tx[e] = A::add(x[e], x[e]);
       }
 #pragma unroll
       for (int e = 0; e < EPL; ++e)
-        if (wr[e]) dst[e][n[e]] = cur[e];
+        if (wr[e]) dst[e][neff[e]] = cur[e];
       // recursion steps m = wmax-1 .. 0: enter the unrolled chain once through
       // a jump table (wmax is warp-uniform) instead of testing every step
       // one predicate per element and step: elements that are not written
       // here (deferred, padding) take no steps (their cur is never used)
-      int neff[EPL];
-#pragma unroll
-      for (int e = 0; e < EPL; ++e) neff[e] = wr[e] ? n[e] : 0;
+      if (!kTwoSets) advance();                  // x, n, goff are dead from here
 #define BOYS_STEP(M)                                                       \
   if ((M) < NB) {                                                           \
     T nx[EPL];                                                              \
@@ -389,13 +394,32 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
       if (body > 0) {
         fence_proxy_async_smem();
         __syncwarp();
-        if (lane == 0) bulk_store(out + base + head, W.stage + shift + head, body * sizeof(T));
+        // operands through warp reductions (identical on every lane): they
+        // land in uniform registers, which the bulk-copy instruction takes,
+        // without the vector-to-uniform waterfall loop
+        const uintptr_t g = reinterpret_cast<uintptr_t>(out + base + head);
+        const unsigned glo = __reduce_max_sync(kFull, (unsigned)g);
+        const unsigned ghi = __reduce_max_sync(kFull, (unsigned)(g >> 32));
+        const unsigned sa = __reduce_max_sync(kFull, smem_u32(W.stage + shift + head));
+        const unsigned nb = __reduce_max_sync(kFull, (unsigned)(body * sizeof(T)));
+        if (lane == 0) bulk_store_u(((uint64_t)ghi << 32) | glo, sa, nb);
       }
     }
-    while (qn >= 32) ragged_drain<T, NB>(W, rows, qn, lane, out);
+    while (qn >= 32) qn = ragged_drain<T, NB>(W, rows, qn, X, NM, OFF, out);
   }
-  while (qn > 0) ragged_drain<T, NB>(W, rows, qn, lane, out);
+  while (qn > 0) qn = ragged_drain<T, NB>(W, rows, qn, X, NM, OFF, out);
   if (lane == 0) bulk_wait_all();
+  // the batch's last, partial chunk: per element, by the warp whose sequence
+  // of chunks reaches it
+  if (c == nfull && nfull * CH < N) {
+#pragma unroll 1
+    for (int e = 0; e < EPL; ++e) {
+      const int64_t j = nfull * CH + 32 * e + lane;
+      const bool jin = j < N;
+      ragged_general_element<T>(jin ? ldg_nc(X + j) : T(0), jin ? (int)NM[j] : 0,
+                                jin ? __ldg(OFF + j) : 0, jin, j, out, dom);
+    }
+  }
 }
 
 // (A block-window ragged variant -- 1024-element windows counting-sorted into
