@@ -35,10 +35,12 @@ struct RaggedWarp {
   static constexpr int CAP = 32 * EPL * (CPE < NB + 1 ? CPE : NB + 1);
   static constexpr int QCAP = 32 * EPL + 32;      // < 32 left after a drain + one chunk
   alignas(16) T stage[CAP + 16 / sizeof(T)];
-  // deferred elements, by index: the drain reloads x, order and offset (cache
-  // hits: the chunk pass has just read them) and recomputes e^{-x}.  One store
-  // per element slot in the chunk pass instead of four (x, t, order, offset).
-  int64_t qidx[QCAP];
+  // deferred elements: x and (offset << 8 | order); the drain recomputes
+  // e^{-x}.  Two stores per element slot in the chunk pass (x, t, order and
+  // offset separately: four; the element index alone: one, but the drain's
+  // dependent reloads then showed up as long-scoreboard stalls).
+  T qx[QCAP];
+  int64_t qon[QCAP];
   T scratch[32];
 };
 
@@ -62,9 +64,7 @@ template <typename T> constexpr bool kDeferUp = sizeof(T) == 4;
 // ~7 chunks of an ERI-like batch, and inlined into the chunk loop its
 // constants (22 uniform loads) and registers were paid on every chunk.
 template <typename T, int NB, typename WarpT>
-__device__ __noinline__ int ragged_drain(WarpT& W, SmemRows<T> st, int qn, const T* __restrict__ X,
-                                         const uint8_t* __restrict__ NM,
-                                         const int64_t* __restrict__ OFF, T* __restrict__ out) {
+__device__ __noinline__ int ragged_drain(WarpT& W, SmemRows<T> st, int qn, T* __restrict__ out) {
   const int lane = threadIdx.x & 31;
   // queued elements' slots were written (with stale staging data) by earlier
   // bulk stores of their chunks: those must be complete before we overwrite
@@ -72,10 +72,11 @@ __device__ __noinline__ int ragged_drain(WarpT& W, SmemRows<T> st, int qn, const
   __syncwarp();
   const int take = qn < 32 ? qn : 32;
   const bool has = lane < take;
-  const int64_t idx = has ? W.qidx[qn - take + lane] : 0;   // LIFO: the newest `take` entries
-  const T x = has ? ldg_nc(X + idx) : T(0);
-  const int n = has ? (int)NM[idx] : 0;
-  const int64_t off = has ? __ldg(OFF + idx) : 0;
+  const int slot = qn - take + lane;            // LIFO: the newest `take` entries
+  const T x = has ? W.qx[slot] : T(0);
+  const int64_t on = has ? W.qon[slot] : 0;
+  const int n = (int)(on & 0xff);
+  const int64_t off = on >> 8;
   const T t = exp_neg_select(x);
   __syncwarp();
   // queued: below the cut-off (Q~ branch) or above x_up (asymptotic branch,
@@ -273,7 +274,8 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
       const unsigned dmask = __ballot_sync(kFull, defer);
       dst[e] = W.stage + (int)(goff[e] - base) + shift;
       const int slot = qn + __popc(dmask & lt_mask);
-      psts(defer, &W.qidx[slot], il + 32 * e);
+      psts(defer, &W.qx[slot], x[e]);
+      psts(defer, &W.qon[slot], (goff[e] << 8) | n[e]);
       qn += __popc(dmask);
       wr[e] = !defer;
       wmax_l = max(wmax_l, defer ? 0 : n[e]);
@@ -405,9 +407,9 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
         if (lane == 0) bulk_store_u(((uint64_t)ghi << 32) | glo, sa, nb);
       }
     }
-    while (qn >= 32) qn = ragged_drain<T, NB>(W, rows, qn, X, NM, OFF, out);
+    while (qn >= 32) qn = ragged_drain<T, NB>(W, rows, qn, out);
   }
-  while (qn > 0) qn = ragged_drain<T, NB>(W, rows, qn, X, NM, OFF, out);
+  while (qn > 0) qn = ragged_drain<T, NB>(W, rows, qn, out);
   if (lane == 0) bulk_wait_all();
   // the batch's last, partial chunk: per element, by the warp whose sequence
   // of chunks reaches it
