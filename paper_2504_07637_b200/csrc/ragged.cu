@@ -688,7 +688,15 @@ static boys_status launch_ragged(const void* x, const uint8_t* nm, const int64_t
 #define BOYS_AB_F64_MINB 0
 #endif
     constexpr int MINB = sizeof(T) == 8 ? BOYS_AB_F64_MINB : BOYS_AB_F32_MINB;
-    boys_status st = launch_chunks<T, NB, EPL, CPE, MINB>(x, nm, off, N, out, dom, s);
+#ifndef BOYS_AB_WT64
+#define BOYS_AB_WT64 kThreads
+#endif
+#ifndef BOYS_AB_CPE64
+#define BOYS_AB_CPE64 BOYS_AB_CPE
+#endif
+    constexpr int WT = sizeof(T) == 8 ? BOYS_AB_WT64 : kThreads;
+    constexpr int CPEw = sizeof(T) == 8 ? BOYS_AB_CPE64 : CPE;
+    boys_status st = launch_chunks<T, NB, EPL, CPEw, MINB, WT>(x, nm, off, N, out, dom, s);
     if (st != BOYS_OK) return st;
   }
   g_launches.fetch_add(1, std::memory_order_relaxed);
