@@ -35,7 +35,7 @@ struct RaggedWarp {
   static constexpr int CAP = 32 * EPL * (CPE < NB + 1 ? CPE : NB + 1);
   static constexpr int QCAP = 32 * EPL + 32;      // < 32 left after a drain + one chunk
   alignas(16) T stage[CAP + 16 / sizeof(T)];
-  // deferred elements: x and (offset << 8 | order); the drain recomputes
+  // deferred elements: x and (order << 56 | offset); the drain recomputes
   // e^{-x}.  Two stores per element slot in the chunk pass (x, t, order and
   // offset separately: four; the element index alone: one, but the drain's
   // dependent reloads then showed up as long-scoreboard stalls).
@@ -75,8 +75,8 @@ __device__ __noinline__ int ragged_drain(WarpT& W, SmemRows<T> st, int qn, T* __
   const int slot = qn - take + lane;            // LIFO: the newest `take` entries
   const T x = has ? W.qx[slot] : T(0);
   const int64_t on = has ? W.qon[slot] : 0;
-  const int n = (int)(on & 0xff);
-  const int64_t off = on >> 8;
+  const int n = (int)(on >> 56);
+  const int64_t off = on & ((int64_t(1) << 56) - 1);
   const T t = exp_neg_select(x);
   __syncwarp();
   // queued: below the cut-off (Q~ branch) or above x_up (asymptotic branch,
@@ -275,7 +275,7 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
       dst[e] = W.stage + (int)(goff[e] - base) + shift;
       const int slot = qn + __popc(dmask & lt_mask);
       psts(defer, &W.qx[slot], x[e]);
-      psts(defer, &W.qon[slot], (goff[e] << 8) | n[e]);
+      psts(defer, &W.qon[slot], goff[e] | ((int64_t)n[e] << 56));   // one op on the high word
       qn += __popc(dmask);
       wr[e] = !defer;
       wmax_l = max(wmax_l, defer ? 0 : n[e]);
