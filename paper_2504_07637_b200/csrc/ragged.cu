@@ -13,15 +13,19 @@ namespace boys {
 // ---------------------------------------------------------------------------
 // ragged kernel: element i, order n_i, values at out[offsets[i] + m]
 //
-// Warp-autonomous (no block barriers): each warp walks chunks of 32*EPL elements.
+// Warp-autonomous (no block barriers): each warp walks full chunks of 32*EPL
+// elements (the batch's last partial chunk goes per element at the end).
 //   * every lane: e^{-x}; elements past their cut-off (x >= z_{n_i}, ~95% of
 //     ERI-like batches) run the cheap run-time-order tail at once into the
-//     warp's staging slot; the chunk's contiguous output range then leaves
-//     with coalesced streaming stores (skipping deferred elements).
+//     warp's staging slot -- seed, then the recursion entered once through a
+//     jump table on the warp's maximum order -- and the chunk's contiguous
+//     output range leaves as one bulk copy (plus scalar head/tail elements).
 //   * elements below their cut-off are deferred to a warp-private queue and
 //     evaluated 32 at a time with every lane busy (Q~ is the expensive part),
-//     each lane writing its element's n+1 values directly.
+//     each lane writing its element's n+1 values directly (ragged_drain).
 // Values are bit-identical to boys_eval_dense at each element's order.
+// The kernel is instruction-issue bound (ncu: DRAM bytes = algorithmic bytes);
+// what the round-2 profiles changed is listed in DESIGN.md section 5.
 // ---------------------------------------------------------------------------
 // EPL elements per lane (chunks of 32*EPL elements): the warp-uniform work of
 // a chunk (ballots, jump-table dispatch, bulk store, constant loads) is shared
@@ -662,14 +666,16 @@ static boys_status launch_ragged(const void* x, const uint8_t* nm, const int64_t
   // in-kernel per-element fallback path
   constexpr int NB = Tab<T>::MAX_ORDER < kRaggedFastOrders ? Tab<T>::MAX_ORDER : kRaggedFastOrders;
   {
-    // (order-sorted warp super-chunks were measured slower: 2.90 / 3.79 ms vs 2.42)
-    // elements per lane: measured best 3 (f64: 1.95 ms vs 2.27 / 1.97 / 2.05
-    // for 1 / 2 / 4) and 4 (f32: 1.14 ms vs 1.26 / 1.16 / 1.36 for 2 / 3 / 6)
-    // elements per lane: measured best 3 (f64: 1.95 ms vs 2.27 / 1.97 / 2.05
-    // for 1 / 2 / 4) and 4 (f32: 1.14 ms vs 1.26 / 1.16 / 1.36 for 2 / 3 / 6);
-    // 12 staged values per element (8: 1.96 ms f64; 2 elements x 10 values,
-    // 24 warps/SM: within 1% but overflows to the slow path from order 10;
-    // 128-thread blocks / 96-register bound: f64 1.84-2.36 vs 1.78 ms)
+    // Same-box A/Bs on cfg4 (tools/ragged_rate.py), current kernel:
+    //  * elements per lane: 3 (f64; 2: 1.64-1.70 vs 1.50 ms, also with three
+    //    resident blocks) and 4 (f32; 3: 0.77-0.78 vs 0.75 ms; 4 with four
+    //    resident blocks spills: 0.95 ms);
+    //  * 12 staged values per element; 256-thread blocks (f64 192 threads x 3
+    //    blocks: 1.59 ms, 128 x 4: 1.50 ms vs 1.43 ms);
+    //  * order-sorted rounds were costed from the profile and not built: the
+    //    recursion is 6 instructions per element and step, a single-slot step
+    //    costs ~11 with its loop, so sorting 96 elements buys less than its
+    //    ballots and shared-memory permutation cost.
 #ifndef BOYS_AB_EPL64
 #define BOYS_AB_EPL64 3
 #endif
@@ -680,23 +686,7 @@ static boys_status launch_ragged(const void* x, const uint8_t* nm, const int64_t
 #define BOYS_AB_CPE 12
 #endif
     constexpr int EPL = sizeof(T) == 8 ? BOYS_AB_EPL64 : BOYS_AB_EPL32, CPE = BOYS_AB_CPE;
-    // fp32: three resident blocks (80 registers)
-#ifndef BOYS_AB_F32_MINB
-#define BOYS_AB_F32_MINB 0
-#endif
-#ifndef BOYS_AB_F64_MINB
-#define BOYS_AB_F64_MINB 0
-#endif
-    constexpr int MINB = sizeof(T) == 8 ? BOYS_AB_F64_MINB : BOYS_AB_F32_MINB;
-#ifndef BOYS_AB_WT64
-#define BOYS_AB_WT64 kThreads
-#endif
-#ifndef BOYS_AB_CPE64
-#define BOYS_AB_CPE64 BOYS_AB_CPE
-#endif
-    constexpr int WT = sizeof(T) == 8 ? BOYS_AB_WT64 : kThreads;
-    constexpr int CPEw = sizeof(T) == 8 ? BOYS_AB_CPE64 : CPE;
-    boys_status st = launch_chunks<T, NB, EPL, CPEw, MINB, WT>(x, nm, off, N, out, dom, s);
+    boys_status st = launch_chunks<T, NB, EPL, CPE, 0>(x, nm, off, N, out, dom, s);
     if (st != BOYS_OK) return st;
   }
   g_launches.fetch_add(1, std::memory_order_relaxed);
