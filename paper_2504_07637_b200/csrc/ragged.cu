@@ -388,7 +388,9 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
     }
     __syncwarp();
     // the chunk's output range [base, base + cnt): scalar head/tail to reach
-    // 16-byte alignment, one bulk async copy (TMA engine) for the body.
+    // 16-byte alignment, one bulk async copy (TMA engine) for the body
+    // (16-byte vector stores by all lanes instead: 1.55 vs 1.42 ms f64, 0.81 vs
+    // 0.76 ms f32).
     // Deferred elements' slots go out stale and are rewritten by the drain.
     {
       const int ncnt = (int)cnt;
