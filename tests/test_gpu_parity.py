@@ -185,6 +185,30 @@ def test_ragged_bit_exact_and_equals_dense(oracle, dtype, cap):
 
 
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_ragged_chunk_loop_sizes(oracle, dtype):
+    """The chunk loop's edges: empty batch, less than one chunk (only the
+    per-element tail runs), exact multiples of the chunk (96 / 128 elements)
+    and one element either side, and a batch larger than the persistent grid
+    (several chunks per warp, the partial chunk owned by a mid-grid warp).
+    ERI-like order mix, so the queue, the drain and the bulk stores all run."""
+    ch = 96 if dtype == np.float64 else 128
+    mx = min(max_order(dtype), 12)
+    rng = np.random.default_rng(17)
+    big = ch * 8 * 148 * 7 + 61                      # > 2 blocks/SM x 8 warps x 148 SMs chunks
+    for N in (0, 1, 31, ch - 1, ch, ch + 1, 5 * ch, 5 * ch + 1, 64 * ch - 1, big):
+        x = np.ascontiguousarray(dense_inputs(dtype, mx, N=max(N, 1))[:N])
+        if N > 4096:                                  # mostly past the cut-off, like cfg4
+            x[::2] = (rng.uniform(40.0, 5000.0, size=x[::2].size)).astype(dtype)
+        w = 1.0 / (np.arange(mx + 1) + 1.0)
+        nm = rng.choice(mx + 1, size=N, p=w / w.sum()).astype(np.uint8)
+        got, off = boys_ragged(torch.from_numpy(x).cuda(), torch.from_numpy(nm).cuda())
+        ref, roff, bad = oracle.ragged(x, nm)
+        assert bad == -1, N
+        assert np.array_equal(off.cpu().numpy(), roff), N
+        assert_parity(got.cpu().numpy(), ref, f"ragged N={N} {dtype.__name__}")
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
 def test_ragged_uniform_orders_staging_capacity(oracle, dtype):
     """Chunks whose output range fills the warp staging exactly (12 values per
     element) or overflows it (orders 12..16: per-element direct-write path),
