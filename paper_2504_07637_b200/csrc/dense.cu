@@ -33,6 +33,7 @@ dense_soa_pair_kernel(const T* __restrict__ X, int64_t N, T* __restrict__ out,
   const int tid = threadIdx.x;
   constexpr int TILE = 2 * kThreads;
   const int64_t ntiles = (N + TILE - 1) / TILE;
+  prefetch_first_tile(X, N, TILE);
   pdl_wait_and_release();
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t i = tile * TILE + 2 * tid;     // even; N even => i + 1 < N iff i < N
@@ -79,6 +80,7 @@ dense_soa_quad_kernel(const T* __restrict__ X, int64_t N, T* __restrict__ out,
   const int tid = threadIdx.x;
   constexpr int TILE = 4 * kThreads;
   const int64_t ntiles = (N + TILE - 1) / TILE;
+  prefetch_first_tile(X, N, TILE);
   pdl_wait_and_release();
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t i = tile * TILE + 4 * tid;     // N % 4 == 0 => all four in range iff i < N
@@ -141,6 +143,7 @@ dense_aos_vec_kernel(const T* __restrict__ X, int64_t N, T* __restrict__ out,
   const int tid = threadIdx.x;
   constexpr int TILE = P * kThreads;
   const int64_t ntiles = (N + TILE - 1) / TILE;
+  prefetch_first_tile(X, N, TILE);
   pdl_wait_and_release();
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t i = tile * TILE + P * tid;     // N % P == 0 => all P in range iff i < N
