@@ -258,19 +258,29 @@ __device__ __forceinline__ void seed_multi_fast(const double (&x)[P], const doub
 // P points per thread in lockstep (generalises eval_pair_stream; per point the
 // same operation sequence as eval_point_stream).  put(m, v[P]) gets F_m of all
 // P points; put1(j, m, v) the upward-ladder values of point j.
+// `any_bad`: warp-uniform, false only if every ok[] of the warp is true; the
+// NaN selects for invalid points then sit behind one uniform branch instead
+// of running for every point (bad points carry x = NaN, for which every
+// comparison below is false, so the ok[] tests fold into the comparisons).
 template <typename T, int n, int P, bool FAST = false, typename Put, typename Put1>
 __device__ __forceinline__ void eval_multi_stream(const T (&xin)[P], const bool (&ok)[P],
-                                                  T (&tout)[P], Put&& put, Put1&& put1) {
+                                                  T (&tout)[P], Put&& put, Put1&& put1,
+                                                  bool any_bad = true) {
   using A = Ar<T>;
   const BoysRow<T>& R = Tab<T>::row(n);
   const T bad = A::nan();
   T x[P], t[P], cur[P], tx[P];
   bool below = false, up = false;
 #pragma unroll
+  for (int j = 0; j < P; ++j) x[j] = xin[j];
+  if (any_bad) {
+#pragma unroll
+    for (int j = 0; j < P; ++j) x[j] = ok[j] ? xin[j] : bad;
+  }
+#pragma unroll
   for (int j = 0; j < P; ++j) {
-    x[j] = ok[j] ? xin[j] : bad;
     t[j] = FAST ? exp_neg_select(x[j]) : exp_neg_clamped(x[j]);
-    below = below || (ok[j] && x[j] < R.z);
+    below = below || x[j] < R.z;
   }
   const bool any_below = __any_sync(kFull, below);
   if constexpr (FAST && sizeof(T) == 8) {
@@ -289,12 +299,12 @@ __device__ __forceinline__ void eval_multi_stream(const T (&xin)[P], const bool 
     put(m, cur);
   }
 #pragma unroll
-  for (int j = 0; j < P; ++j) up = up || (ok[j] && x[j] > R.x_up);
+  for (int j = 0; j < P; ++j) up = up || x[j] > R.x_up;
   // n = 0: the ladder's F_0 = c_0 sqrt(1/x) is the y = x seed itself
   if (n > 0 && __any_sync(kFull, up)) {
 #pragma unroll
     for (int j = 0; j < P; ++j) {
-      const bool upj = ok[j] && x[j] > R.x_up;
+      const bool upj = x[j] > R.x_up;
       T rx = A::rcp(x[j]);
       T f = up_first(x[j]);
       if (upj) put1(j, 0, f);
@@ -306,7 +316,11 @@ __device__ __forceinline__ void eval_multi_stream(const T (&xin)[P], const bool 
     }
   }
 #pragma unroll
-  for (int j = 0; j < P; ++j) tout[j] = ok[j] ? t[j] : bad;
+  for (int j = 0; j < P; ++j) tout[j] = t[j];
+  if (any_bad) {
+#pragma unroll
+    for (int j = 0; j < P; ++j) tout[j] = ok[j] ? t[j] : bad;
+  }
 }
 
 template <typename T, int n, bool FAST = false, typename Put, typename Put1>

@@ -94,16 +94,24 @@ dense_soa_quad_kernel(const T* __restrict__ X, int64_t N, T* __restrict__ out,
     } else {
       xv[0] = xv[1] = xv[2] = xv[3] = T(0);
     }
+    // one 32-bit compare per point (positive, finite); anything else -- -0.0
+    // included, which is valid -- is settled behind one vote per thread
     bool bad = false;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      ok[j] = valid_x(xv[j]) || !in;
+      ok[j] = surely_valid_x(xv[j]);
       bad = bad || !ok[j];
     }
-    if (__any_sync(kFull, bad)) {                  // rare: one vote per thread, not a branch per point
+    bool any_bad = __any_sync(kFull, bad);
+    if (any_bad) {                                 // rare
+      bad = false;
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
+      for (int j = 0; j < 4; ++j) {
+        ok[j] = valid_x(xv[j]) || !in;
+        bad = bad || !ok[j];
         if (!ok[j]) flag_domain(dom, index_base + i + j);
+      }
+      any_bad = __any_sync(kFull, bad);
     }
     T* o = out + i;
     T tv[4];
@@ -119,7 +127,8 @@ dense_soa_quad_kernel(const T* __restrict__ X, int64_t N, T* __restrict__ out,
         },
         [&](int j, int m, T v) {
           if (in) __stcs(o + (int64_t)m * N + j, v);
-        });
+        },
+        any_bad);
     if (expx && in) {
       V2 a, b;
       a.x = tv[0]; a.y = tv[1]; b.x = tv[2]; b.y = tv[3];
