@@ -138,6 +138,119 @@ dense_soa_quad_kernel(const T* __restrict__ X, int64_t N, T* __restrict__ out,
   }
 }
 
+// Four points of a thread at n = 0: domain check, F_0 and e^{-x} into
+// registers (shared by the speculative kernel below and its cold re-run).
+template <typename T>
+__device__ __forceinline__ void quad0_eval(const T (&xv)[4], bool in, T (&fv)[4], T (&tv)[4],
+                                           bool (&ok)[4], bool& any_bad) {
+  bool bad = false;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    ok[j] = surely_valid_x(xv[j]);
+    bad = bad || !ok[j];
+  }
+  any_bad = __any_sync(kFull, bad);
+  if (any_bad) {                                   // rare
+    bad = false;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      ok[j] = valid_x(xv[j]) || !in;
+      bad = bad || !ok[j];
+    }
+    any_bad = __any_sync(kFull, bad);
+  }
+  eval_multi_stream<T, 0, 4, true>(
+      xv, ok, tv,
+      [&](int, const T (&v)[4]) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) fv[j] = v[j];
+      },
+      [&](int, int, T) {}, any_bad);
+}
+
+template <typename T>
+__device__ __forceinline__ void quad0_store(const T (&fv)[4], const T (&tv)[4], const bool (&ok)[4],
+                                            bool any_bad, bool in, int64_t i, T* __restrict__ out,
+                                            T* __restrict__ expx, int64_t* __restrict__ dom,
+                                            int64_t index_base) {
+  using V2 = typename std::conditional<sizeof(T) == 8, double2, float2>::type;
+  if (any_bad) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (!ok[j]) flag_domain(dom, index_base + i + j);
+  }
+  if (in) {
+    V2 a, b;
+    a.x = fv[0]; a.y = fv[1]; b.x = fv[2]; b.y = fv[3];
+    __stcs(reinterpret_cast<V2*>(out + i), a);
+    __stcs(reinterpret_cast<V2*>(out + i + 2), b);
+    if (expx) {
+      a.x = tv[0]; a.y = tv[1]; b.x = tv[2]; b.y = tv[3];
+      __stcs(reinterpret_cast<V2*>(expx + i), a);
+      __stcs(reinterpret_cast<V2*>(expx + i + 2), b);
+    }
+  }
+}
+
+// n = 0 variant of the four-point SoA kernel that computes BEFORE waiting on
+// the stream's previous grid: each block loads its x tile and evaluates F_0
+// into registers while the previous grid's tail is still draining, then
+// waits (griddepcontrol.wait: the previous grid has completed and its writes
+// are visible), re-reads x past L1 and compares bit for bit.  Equal (x was not
+// produced by the previous grid -- the usual case): the results are stored.
+// Different: the tile is evaluated again, now after the wait.  Nothing
+// is written and no domain flag is raised before the wait, so the launch stays
+// stream-ordered for every buffer; the only early accesses are reads of x,
+// whose values are confirmed afterwards.  One row of results (8 registers) is
+// held across the wait, which is why only n = 0 does this.  A stream of
+// 2^20-point launches keeps the FP64 pipe busy across launch boundaries.
+template <typename T, int MINB, bool EXPX>
+__global__ void __launch_bounds__(kThreads, MINB)
+dense_soa_quad0_spec_kernel(const T* __restrict__ X, int64_t N, T* __restrict__ out,
+                            T* __restrict__ expx_arg, int64_t* __restrict__ dom,
+                            int64_t index_base) {
+  T* __restrict__ expx = EXPX ? expx_arg : nullptr;  // without it the e^{-x} row is dead code
+  using V2 = typename std::conditional<sizeof(T) == 8, double2, float2>::type;
+  const int tid = threadIdx.x;
+  constexpr int TILE = 4 * kThreads;
+  const int64_t ntiles = (N + TILE - 1) / TILE;
+  // dependents wait for this grid's completion themselves before they store
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  bool waited = false;                             // block-uniform
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t i = tile * TILE + 4 * tid;     // N % 4 == 0 => all four in range iff i < N
+    const bool in = i < N;
+    V2 xa, xb;
+    xa.x = xa.y = xb.x = xb.y = T(0);
+    if (in) {
+      xa = __ldcg(reinterpret_cast<const V2*>(X + i));
+      xb = __ldcg(reinterpret_cast<const V2*>(X + i + 2));
+    }
+    const T xv[4] = {xa.x, xa.y, xb.x, xb.y};
+    T fv[4], tv[4];
+    bool ok[4], any_bad;
+    quad0_eval<T>(xv, in, fv, tv, ok, any_bad);
+    if (!waited) {
+      asm volatile("griddepcontrol.wait;\n" ::: "memory");
+      waited = true;
+      const V2 pa = xa, pb = xb;
+      V2 ya = pa, yb = pb;
+      if (in) {
+        ya = __ldcg(reinterpret_cast<const V2*>(X + i));
+        yb = __ldcg(reinterpret_cast<const V2*>(X + i + 2));
+      }
+      const bool diff = !same_bits(ya.x, pa.x) || !same_bits(ya.y, pa.y) ||
+                        !same_bits(yb.x, pb.x) || !same_bits(yb.y, pb.y);
+      if (__any_sync(kFull, diff)) {               // speculation failed: this tile again, now after the wait
+        tile -= gridDim.x;
+        continue;
+      }
+    }
+    quad0_store<T>(fv, tv, ok, any_bad, in, i, out, expx, dom, index_base);
+  }
+  if (!waited) asm volatile("griddepcontrol.wait;\n" ::: "memory");
+}
+
 // AoS dense kernel for rows of 2 or 4 values (n = 1, 3): P adjacent points per
 // thread, each point's row kept in registers and written straight to global
 // memory as 16-byte vectors (the thread's P rows are contiguous), no shared
@@ -392,8 +505,22 @@ static boys_status launch_soa_pair(const T* x, int64_t N, T* out, T* expx, int64
 template <typename T, int n>
 static boys_status launch_soa_quad(const T* x, int64_t N, T* out, T* expx, int64_t* dom,
                                    int64_t base, cudaStream_t s) {
-  auto k = dense_soa_quad_kernel<T, n, 4, true>;
   const int64_t ntiles = (N + 4 * kThreads - 1) / (4 * kThreads);
+  // n = 0, up to 2^22 points: the speculative kernel (a stream of 2^20-point
+  // launches: 7.16 vs 7.68 us per launch; three resident blocks, no spills:
+  // four measured 7.29 us).  Larger launches gain nothing at their boundaries
+  // and pay the re-read (2^26 points: +1.2-2.5%), so they keep the plain kernel.
+  if constexpr (n == 0) {
+    if (N <= (int64_t(1) << 22)) {
+      if (expx) {
+        auto k0 = dense_soa_quad0_spec_kernel<T, 3, true>;
+        return launch_pdl(k0, per_tile_grid(k0, 0, ntiles), 0, s, x, N, out, expx, dom, base);
+      }
+      auto k0 = dense_soa_quad0_spec_kernel<T, 3, false>;
+      return launch_pdl(k0, per_tile_grid(k0, 0, ntiles), 0, s, x, N, out, expx, dom, base);
+    }
+  }
+  auto k = dense_soa_quad_kernel<T, n, 4, true>;
   return launch_pdl(k, per_tile_grid(k, 0, ntiles), 0, s, x, N, out, expx, dom, base);
 }
 

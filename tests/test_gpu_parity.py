@@ -325,6 +325,59 @@ def test_stream_ordering_and_launch_count():
     assert _lib.launch_count() >= before + 2
 
 
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_n0_speculative_kernel_is_stream_ordered(oracle, dtype):
+    """The n = 0 kernel (up to 2^22 points) evaluates before it waits on the
+    stream's previous grid and confirms x afterwards.  Chained launches whose
+    x IS the previous launch's output make the speculation fail: every link of
+    the chain must still see its producer's values (F_0 maps [0, inf) into
+    (0, 1], so outputs are valid inputs).  Also through a CUDA graph, where the
+    launches carry programmatic dependency edges, and for an in-place x update
+    by another kernel between two launches."""
+    tdt = torch.float64 if dtype == np.float64 else torch.float32
+    for N in (4096, (1 << 20) + 4, 1 << 22):
+        x0 = W.cfg1_x(N, device="cuda").to(tdt)
+        ref = x0.cpu().numpy()
+        links = 4
+        for _ in range(links):
+            ref, bad = oracle.dense(0, np.ascontiguousarray(ref.reshape(-1)), "soa")
+            assert bad == -1
+        bufs = [torch.full((1, N), 0.5, dtype=tdt, device="cuda") for _ in range(links)]
+
+        def chain():
+            src = x0
+            for b in bufs:
+                boys(0, src.view(-1), out=b, check=False)
+                src = b
+        for rep in range(3):
+            for b in bufs:
+                b.fill_(0.25 + 0.125 * rep)           # stale, valid values for the early reads
+            chain()
+            torch.cuda.synchronize()
+            assert_parity(bufs[-1].cpu().numpy(), ref, f"n=0 chain N={N} rep={rep}")
+        g = torch.cuda.CUDAGraph()
+        for b in bufs:
+            b.fill_(0.75)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g):
+            chain()
+        for rep in range(3):
+            for b in bufs:
+                b.fill_(0.3)
+            g.replay()
+            torch.cuda.synchronize()
+            assert_parity(bufs[-1].cpu().numpy(), ref, f"n=0 graph chain N={N} rep={rep}")
+    # x rewritten in place by another kernel right before the launch
+    x = W.cfg1_x(1 << 20, device="cuda").to(tdt)
+    out = torch.empty((1, x.numel()), dtype=tdt, device="cuda")
+    for rep in range(4):
+        boys(0, x, out=out, check=False)
+        x.mul_(1.5).add_(0.25)
+        boys(0, x, out=out, check=False)
+        want, _ = oracle.dense(0, x.cpu().numpy(), "soa")
+        assert_parity(out.cpu().numpy(), want, f"n=0 after in-place update rep={rep}")
+
+
 def test_cuda_graph_capture_and_replay():
     """Device entry points are stream-ordered and host-sync free, so they can be
     captured into a CUDA graph (the bench's cfg1 stream uses this); replays
