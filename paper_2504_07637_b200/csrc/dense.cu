@@ -208,7 +208,7 @@ template <typename T, int MINB, bool EXPX>
 __global__ void __launch_bounds__(kThreads, MINB)
 dense_soa_quad0_spec_kernel(const T* __restrict__ X, int64_t N, T* __restrict__ out,
                             T* __restrict__ expx_arg, int64_t* __restrict__ dom,
-                            int64_t index_base) {
+                            int64_t index_base, int ahead) {
   T* __restrict__ expx = EXPX ? expx_arg : nullptr;  // without it the e^{-x} row is dead code
   using V2 = typename std::conditional<sizeof(T) == 8, double2, float2>::type;
   const int tid = threadIdx.x;
@@ -226,6 +226,15 @@ dense_soa_quad0_spec_kernel(const T* __restrict__ X, int64_t N, T* __restrict__ 
       xa = __ldcg(reinterpret_cast<const V2*>(X + i));
       xb = __ldcg(reinterpret_cast<const V2*>(X + i + 2));
     }
+#ifndef BOYS_AB_NOAHEAD
+    // L2 prefetch for the block that takes this one's place (`ahead` = resident
+    // blocks of the grid): the next wave starts all at once when this one
+    // leaves, and would otherwise open with a DRAM round trip
+    if (tile + ahead < ntiles) {
+      constexpr int PER = 32 / (int)sizeof(T);
+      if (tid * PER < TILE) prefetch_l2(X + (tile + ahead) * TILE + tid * PER);
+    }
+#endif
     const T xv[4] = {xa.x, xa.y, xb.x, xb.y};
     T fv[4], tv[4];
     bool ok[4], any_bad;
@@ -514,10 +523,12 @@ static boys_status launch_soa_quad(const T* x, int64_t N, T* out, T* expx, int64
     if (N <= (int64_t(1) << 22)) {
       if (expx) {
         auto k0 = dense_soa_quad0_spec_kernel<T, 3, true>;
-        return launch_pdl(k0, per_tile_grid(k0, 0, ntiles), 0, s, x, N, out, expx, dom, base);
+        const int ahead = blocks_for(k0, 0, int64_t(1) << 40);     // resident blocks
+        return launch_pdl(k0, per_tile_grid(k0, 0, ntiles), 0, s, x, N, out, expx, dom, base, ahead);
       }
       auto k0 = dense_soa_quad0_spec_kernel<T, 3, false>;
-      return launch_pdl(k0, per_tile_grid(k0, 0, ntiles), 0, s, x, N, out, expx, dom, base);
+      const int ahead = blocks_for(k0, 0, int64_t(1) << 40);
+      return launch_pdl(k0, per_tile_grid(k0, 0, ntiles), 0, s, x, N, out, expx, dom, base, ahead);
     }
   }
   auto k = dense_soa_quad_kernel<T, n, 4, true>;
