@@ -36,7 +36,7 @@ def ncu_ms(sub):
 
 
 ALG = "algorithmic_bytes_per_launch"
-KER = {"cfg3": "dense_kernel<double, 16", "cfg1": "dense_soa_quad_kernel<double, 0", "cfg2": "dense_soa_pair_kernel<double, 8",
+KER = {"cfg3": "dense_kernel<double, 16", "cfg1": "dense_soa_quad0_spec_kernel<double", "cfg2": "dense_soa_pair_kernel<double, 8",
        "cfg4": "ragged_kernel<double", "cfg4f32": "ragged_kernel<float", "cfg5": "dense_kernel<double, 12",
        "split": "split_kernel<double, 16", "hermite": "hermite_kernel<4>"}
 rf, ck = b["roofline"], b["clocks"]
