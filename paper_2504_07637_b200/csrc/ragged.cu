@@ -675,6 +675,10 @@ static boys_status launch_ragged(const void* x, const uint8_t* nm, const int64_t
     //  * 12 staged values per element; 256-thread blocks (f64 192 threads x 3
     //    blocks: 1.59 ms, 128 x 4: 1.50 ms vs 1.43 ms); f64 at three resident
     //    blocks (8 staged values, 80 registers, spills): 1.65-1.72 vs 1.42 ms;
+    //  * f64 recursion aligned at the chain start (no select on `cur`; the
+    //    per-lane RN(1/(2M+1)) from shared memory one step ahead): ptxas copies
+    //    the prefetched multipliers at every jump-table label (6 moves per
+    //    step that wait on the loads): 1.67 vs 1.42 ms;
     //  * order-sorted rounds were costed from the profile and not built: the
     //    recursion is 6 instructions per element and step, a single-slot step
     //    costs ~11 with its loop, so sorting 96 elements buys less than its
