@@ -29,6 +29,13 @@
  *     is stream-ordered on `stream` (a cudaStream_t passed as void*; NULL =
  *     legacy default stream).  No allocation and no host sync on the device
  *     entry points; tables are compiled into the module (__constant__).
+ *     Kernels launch with programmatic stream serialization: a launch may
+ *     begin (and boys_eval_dense at n_max = 0 may read x and evaluate) while
+ *     the stream's previous kernel is still draining, but it writes nothing
+ *     before that kernel has completed, and it re-reads x afterwards and
+ *     re-evaluates if a value changed -- results are those of a fully
+ *     serialized launch.  x must be a mapped device buffer when the call is
+ *     made (it always is for memory the caller owns at that point).
  *   - Layouts: BOYS_SOA = order-major [n_max+1][N]; BOYS_AOS = point-major
  *     [N][n_max+1] ("order-major, point-major").
  *   - Domain: x must be finite and >= 0 (-0.0 is accepted as 0).  Offending
