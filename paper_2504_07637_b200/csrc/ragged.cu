@@ -679,6 +679,8 @@ static boys_status launch_ragged(const void* x, const uint8_t* nm, const int64_t
     //    per-lane RN(1/(2M+1)) from shared memory one step ahead): ptxas copies
     //    the prefetched multipliers at every jump-table label (6 moves per
     //    step that wait on the loads): 1.67 vs 1.42 ms;
+    //  * the chunk loop unrolled by two (no register copies between the two
+    //    sets; 120 registers, twice the code): 1.75 vs 1.42 ms;
     //  * order-sorted rounds were costed from the profile and not built: the
     //    recursion is 6 instructions per element and step, a single-slot step
     //    costs ~11 with its loop, so sorting 96 elements buys less than its
