@@ -11,6 +11,7 @@ timeout 600 ncu --set full --clock-control none --import-source on -f -k regex:"
 echo "ncu $cfg rc=$?"
 ncu -i /tmp/prof_$cfg.ncu-rep --page source --csv > /tmp/src_$cfg.csv 2>/dev/null
 ncu -i /tmp/prof_$cfg.ncu-rep --page raw --csv > gpurun_out/raw_$cfg.csv 2>/dev/null
+cp /tmp/src_$cfg.csv gpurun_out/src_$cfg.csv; gzip -f gpurun_out/src_$cfg.csv; cp /tmp/${unit}_gi.txt gpurun_out/${unit}_gi.txt; gzip -f gpurun_out/${unit}_gi.txt
 python tools/ncu_keys.py gpurun_out/raw_$cfg.csv | tee gpurun_out/keys_$cfg.txt
 F=$(grep -o "^\.text\.[A-Za-z0-9_]*$sub[A-Za-z0-9_]*" /tmp/$unit.txt | head -1 | sed 's/^\.text\.//')
 python tools/sass_lines.py /tmp/src_$cfg.csv /tmp/$unit.txt $F "$kre" 60 > gpurun_out/lines_$cfg.txt 2>&1
