@@ -145,7 +145,11 @@ template <typename T, int n, bool AOS>
 static boys_status launch_split_t(const T* x, int64_t N, int nbar, T* out, int64_t* dom,
                                   cudaStream_t s) {
   constexpr bool fits2 = 2 * kThreads * (n + 1) * sizeof(T) <= 80 * 1024 && !RowStride<n + 1>::padded;
-  constexpr int NBUF = (AOS && fits2) ? 2 : 1;
+  // double-buffered staging below n = 12; from there one buffer and four
+  // resident blocks (two seeds per point: more warps pay more than the second
+  // buffer; same-box 2^24 points: (16, 8) 0.419 vs 0.429 ms, (12, 11) 0.357 vs
+  // 0.361 ms, but (8, 4) 0.320 vs 0.318 ms)
+  constexpr int NBUF = (AOS && fits2 && n < 12) ? 2 : 1;
   // compile-time lower order for the common pairs: n_bar = n - 1 (one more
   // order: "a few more bits") and n_bar = n / 2
   // (orders above 16 only run-time nbar: compile time and library size)
