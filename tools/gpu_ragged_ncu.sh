@@ -1,5 +1,5 @@
 # Ragged kernels: ncu --set full with source, key issue/stall metrics, per-source-line attribution.
-# usage: gpu_r02u.sh [configs...]   (default cfg4 cfg4f32)
+# usage: gpu_ragged_ncu.sh [configs...]   (default cfg4 cfg4f32)
 mkdir -p gpurun_out
 CFGS=${@:-cfg4 cfg4f32}
 cd /tmp && cuobjdump -xelf all $GRAFT_REPO_ROOT/paper_2504_07637_b200/libboys.so > /dev/null 2>&1
