@@ -58,10 +58,10 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
 // tile, one 32-byte sector per thread), issued BEFORE waiting on the stream's
 // previous grid: a cache hint, safe whoever produces x (L2 is the point of
 // coherence), so the first loads after the wait hit L2 with a warm TLB.  A
-// stream of 2^20-point n = 0 launches: 8.29 -> 7.78 us per launch; cfg2 -0.7%.
-// Used by the one-block-per-tile kernels (SoA quad / pair, AoS register rows);
-// in the persistent AoS kernels it measured 0.2-1% slower (cfg3, cfg5) and is
-// not used.
+// stream of 2^20-point n = 0 launches: 8.29 -> 7.78 us per launch (before
+// that config got its speculative kernel); cfg2 -0.7%.  Used by the two-point
+// SoA kernel only: at 2^24 points it cost the four-point SoA kernel 1-4.5%
+// (n = 3..5) and the persistent AoS kernels 0.2-1% (cfg3, cfg5).
 template <typename T>
 __device__ __forceinline__ void prefetch_first_tile(const T* X, int64_t N, int tile) {
   constexpr int PER = 32 / (int)sizeof(T);
@@ -174,7 +174,10 @@ __device__ __forceinline__ void eval_point(T x_in, bool ok, T (&Fv)[n + 1], T& t
 // point of the thread recomputes that operation with it), so the P chains
 // interleave without a branch region per call.  The FP64-bound small orders'
 // multi-point SoA kernels use it.
-template <int n, int P>
+// COLD: the fallbacks as volatile asm (they cannot be speculated above their
+// vote).  Same values either way; it is a code-generation choice measured per
+// kernel (dense.cu), like the kernel rules there.
+template <int n, int P, bool COLD = false>
 __device__ __forceinline__ void seed_multi_fast(const double (&x)[P], const double (&t)[P],
                                                 bool any_below, double (&F)[P]) {
   using A = Ar<double>;
@@ -213,7 +216,7 @@ __device__ __forceinline__ void seed_multi_fast(const double (&x)[P], const doub
     }
     if (__any_sync(kFull, slow)) {
 #pragma unroll
-      for (int j = 0; j < P; ++j) sq[j] = A::sqrt_cold(Q[j]);
+      for (int j = 0; j < P; ++j) sq[j] = COLD ? A::sqrt_cold(Q[j]) : A::sqrt(Q[j]);
     }
 #pragma unroll
     for (int j = 0; j < P; ++j) {
@@ -232,7 +235,7 @@ __device__ __forceinline__ void seed_multi_fast(const double (&x)[P], const doub
   }
   if (__any_sync(kFull, slow)) {
 #pragma unroll
-    for (int j = 0; j < P; ++j) r[j] = A::rcp_cold(y[j]);
+    for (int j = 0; j < P; ++j) r[j] = COLD ? A::rcp_cold(y[j]) : A::rcp(y[j]);
   }
   slow = false;
 #pragma unroll
@@ -243,7 +246,7 @@ __device__ __forceinline__ void seed_multi_fast(const double (&x)[P], const doub
   }
   if (__any_sync(kFull, slow)) {
 #pragma unroll
-    for (int j = 0; j < P; ++j) sr[j] = A::sqrt_cold(r[j]);
+    for (int j = 0; j < P; ++j) sr[j] = COLD ? A::sqrt_cold(r[j]) : A::sqrt(r[j]);
   }
 #pragma unroll
   for (int j = 0; j < P; ++j)
@@ -258,11 +261,13 @@ __device__ __forceinline__ void seed_multi_fast(const double (&x)[P], const doub
 // P points per thread in lockstep (generalises eval_pair_stream; per point the
 // same operation sequence as eval_point_stream).  put(m, v[P]) gets F_m of all
 // P points; put1(j, m, v) the upward-ladder values of point j.
-// `any_bad`: warp-uniform, false only if every ok[] of the warp is true; the
-// NaN selects for invalid points then sit behind one uniform branch instead
-// of running for every point (bad points carry x = NaN, for which every
-// comparison below is false, so the ok[] tests fold into the comparisons).
-template <typename T, int n, int P, bool FAST = false, typename Put, typename Put1>
+// ANYBAD: `any_bad` is a warp-uniform run-time flag, false only if every ok[]
+// of the warp is true; the NaN selects for invalid points then sit behind one
+// uniform branch instead of running for every point (the n = 0 speculative
+// kernel).  Without ANYBAD the selects run per point, as before: the kernels
+// that use that form measured faster with it (dense.cu).
+template <typename T, int n, int P, bool FAST = false, bool ANYBAD = false, bool COLD = false,
+          typename Put, typename Put1>
 __device__ __forceinline__ void eval_multi_stream(const T (&xin)[P], const bool (&ok)[P],
                                                   T (&tout)[P], Put&& put, Put1&& put1,
                                                   bool any_bad = true) {
@@ -271,20 +276,23 @@ __device__ __forceinline__ void eval_multi_stream(const T (&xin)[P], const bool 
   const T bad = A::nan();
   T x[P], t[P], cur[P], tx[P];
   bool below = false, up = false;
+  if constexpr (ANYBAD) {
 #pragma unroll
-  for (int j = 0; j < P; ++j) x[j] = xin[j];
-  if (any_bad) {
+    for (int j = 0; j < P; ++j) x[j] = xin[j];
+    if (any_bad) {
 #pragma unroll
-    for (int j = 0; j < P; ++j) x[j] = ok[j] ? xin[j] : bad;
+      for (int j = 0; j < P; ++j) x[j] = ok[j] ? xin[j] : bad;
+    }
   }
 #pragma unroll
   for (int j = 0; j < P; ++j) {
+    if constexpr (!ANYBAD) x[j] = ok[j] ? xin[j] : bad;
     t[j] = FAST ? exp_neg_select(x[j]) : exp_neg_clamped(x[j]);
-    below = below || x[j] < R.z;
+    below = below || (ok[j] && x[j] < R.z);
   }
   const bool any_below = __any_sync(kFull, below);
   if constexpr (FAST && sizeof(T) == 8) {
-    seed_multi_fast<n, P>(x, t, any_below, cur);
+    seed_multi_fast<n, P, COLD>(x, t, any_below, cur);
   } else {
 #pragma unroll
     for (int j = 0; j < P; ++j) cur[j] = seed<T, n>(x[j], t[j], any_below);
@@ -299,12 +307,12 @@ __device__ __forceinline__ void eval_multi_stream(const T (&xin)[P], const bool 
     put(m, cur);
   }
 #pragma unroll
-  for (int j = 0; j < P; ++j) up = up || x[j] > R.x_up;
+  for (int j = 0; j < P; ++j) up = up || (ok[j] && x[j] > R.x_up);
   // n = 0: the ladder's F_0 = c_0 sqrt(1/x) is the y = x seed itself
   if (n > 0 && __any_sync(kFull, up)) {
 #pragma unroll
     for (int j = 0; j < P; ++j) {
-      const bool upj = x[j] > R.x_up;
+      const bool upj = ok[j] && x[j] > R.x_up;
       T rx = A::rcp(x[j]);
       T f = up_first(x[j]);
       if (upj) put1(j, 0, f);
@@ -315,9 +323,14 @@ __device__ __forceinline__ void eval_multi_stream(const T (&xin)[P], const bool 
       }
     }
   }
+  if constexpr (ANYBAD) {
 #pragma unroll
-  for (int j = 0; j < P; ++j) tout[j] = t[j];
-  if (any_bad) {
+    for (int j = 0; j < P; ++j) tout[j] = t[j];
+    if (any_bad) {
+#pragma unroll
+      for (int j = 0; j < P; ++j) tout[j] = ok[j] ? t[j] : bad;
+    }
+  } else {
 #pragma unroll
     for (int j = 0; j < P; ++j) tout[j] = ok[j] ? t[j] : bad;
   }

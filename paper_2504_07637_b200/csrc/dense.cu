@@ -20,6 +20,9 @@ namespace boys {
 // (n=3..8: 2-12% slower) -- more registers where the kernel is HBM-bound.
 template <typename T, int n> constexpr bool kFastVec = sizeof(T) == 8;
 template <typename T, int n> constexpr bool kFastSoaPair = sizeof(T) == 8 && n >= 11;
+// AoS register rows: the fast paths' fallbacks as volatile asm at n = 3 (f64
+// 2^24 points: 0.154 vs 0.168 ms; n = 1, 2 measured no gain)
+template <int n> constexpr bool kColdVec = n == 3;
 
 // SoA dense kernel, two adjacent points per thread (512-point tiles): x comes
 // in as one 16-byte load and every F_m row leaves as 16-byte streaming stores
@@ -80,7 +83,6 @@ dense_soa_quad_kernel(const T* __restrict__ X, int64_t N, T* __restrict__ out,
   const int tid = threadIdx.x;
   constexpr int TILE = 4 * kThreads;
   const int64_t ntiles = (N + TILE - 1) / TILE;
-  prefetch_first_tile(X, N, TILE);
   pdl_wait_and_release();
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t i = tile * TILE + 4 * tid;     // N % 4 == 0 => all four in range iff i < N
@@ -94,24 +96,16 @@ dense_soa_quad_kernel(const T* __restrict__ X, int64_t N, T* __restrict__ out,
     } else {
       xv[0] = xv[1] = xv[2] = xv[3] = T(0);
     }
-    // one 32-bit compare per point (positive, finite); anything else -- -0.0
-    // included, which is valid -- is settled behind one vote per thread
     bool bad = false;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      ok[j] = surely_valid_x(xv[j]);
+      ok[j] = valid_x(xv[j]) || !in;
       bad = bad || !ok[j];
     }
-    bool any_bad = __any_sync(kFull, bad);
-    if (any_bad) {                                 // rare
-      bad = false;
+    if (__any_sync(kFull, bad)) {                  // rare: one vote per thread, not a branch per point
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        ok[j] = valid_x(xv[j]) || !in;
-        bad = bad || !ok[j];
+      for (int j = 0; j < 4; ++j)
         if (!ok[j]) flag_domain(dom, index_base + i + j);
-      }
-      any_bad = __any_sync(kFull, bad);
     }
     T* o = out + i;
     T tv[4];
@@ -127,8 +121,7 @@ dense_soa_quad_kernel(const T* __restrict__ X, int64_t N, T* __restrict__ out,
         },
         [&](int j, int m, T v) {
           if (in) __stcs(o + (int64_t)m * N + j, v);
-        },
-        any_bad);
+        });
     if (expx && in) {
       V2 a, b;
       a.x = tv[0]; a.y = tv[1]; b.x = tv[2]; b.y = tv[3];
@@ -159,7 +152,7 @@ __device__ __forceinline__ void quad0_eval(const T (&xv)[4], bool in, T (&fv)[4]
     }
     any_bad = __any_sync(kFull, bad);
   }
-  eval_multi_stream<T, 0, 4, true>(
+  eval_multi_stream<T, 0, 4, true, true, true>(
       xv, ok, tv,
       [&](int, const T (&v)[4]) {
 #pragma unroll
@@ -274,7 +267,6 @@ dense_aos_vec_kernel(const T* __restrict__ X, int64_t N, T* __restrict__ out,
   const int tid = threadIdx.x;
   constexpr int TILE = P * kThreads;
   const int64_t ntiles = (N + TILE - 1) / TILE;
-  prefetch_first_tile(X, N, TILE);
   pdl_wait_and_release();
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t i = tile * TILE + P * tid;     // N % P == 0 => all P in range iff i < N
@@ -295,7 +287,7 @@ dense_aos_vec_kernel(const T* __restrict__ X, int64_t N, T* __restrict__ out,
       if (in && !ok[j]) flag_domain(dom, index_base + i + j);
       ok[j] = ok[j] || !in;
     }
-    eval_multi_stream<T, n, P, kFastVec<T, n>>(
+    eval_multi_stream<T, n, P, kFastVec<T, n>, false, kColdVec<n>>(
         xv, ok, tv,
         [&](int m, const T (&v)[P]) {
 #pragma unroll
