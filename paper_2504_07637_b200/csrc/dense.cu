@@ -36,7 +36,10 @@ dense_soa_pair_kernel(const T* __restrict__ X, int64_t N, T* __restrict__ out,
   const int tid = threadIdx.x;
   constexpr int TILE = 2 * kThreads;
   const int64_t ntiles = (N + TILE - 1) / TILE;
-  prefetch_first_tile(X, N, TILE);
+  // pre-wait L2 prefetch (boys_device.cuh): f64 every order (2^24 points: 0 to
+  // -1.6%), f32 where it measured faster (n = 9..11: -3 to -9%, n <= 7: 0 to
+  // -2%; n = 8 and n >= 12 measured +1 to +3% and skip it)
+  if constexpr (sizeof(T) == 8 || (n != 8 && n < 12)) prefetch_first_tile(X, N, TILE);
   pdl_wait_and_release();
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t i = tile * TILE + 2 * tid;     // even; N even => i + 1 < N iff i < N

@@ -10,12 +10,16 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2504_07637_b200 import boys, workloads as W  # noqa: E402
 
 N = 1 << 24
-x = W.cfg3_x(N, device="cuda")
+# optional: dtype (f64 | f32) and "layout:n,n,..." groups, e.g.  f32 soa:6,8,12
+dt = torch.float32 if len(sys.argv) > 1 and sys.argv[1] == "f32" else torch.float64
+groups = [(g.split(":")[0], tuple(int(v) for v in g.split(":")[1].split(","))) for g in sys.argv[2:]] \
+    or [("soa", (0, 1, 2, 3, 4, 5)), ("aos", (1, 2, 3))]
+x = W.cfg3_x(N, device="cuda").to(dt)
 res = {}
-for lay, orders in (("soa", (0, 1, 2, 3, 4, 5)), ("aos", (1, 2, 3))):
+for lay, orders in groups:
     for n in orders:
         shape = (n + 1, N) if lay == "soa" else (N, n + 1)
-        outs = [torch.empty(shape, dtype=torch.float64, device="cuda") for _ in range(2)]
+        outs = [torch.empty(shape, dtype=dt, device="cuda") for _ in range(2)]
         for k in range(3):
             boys(n, x, layout=lay, out=outs[k % 2], check=False)
         torch.cuda.synchronize()
