@@ -5,7 +5,7 @@ timeout 600 python bench.py --steps 5 --warmup 3 --extras hermite,cfg2 --e2e-ste
 python -c "
 import json; d=json.loads(open('gpurun_out/bench_h.jsonl').read().strip().splitlines()[-1])
 print({k:(v.get('value'),v.get('ms_per_step'),v.get('roofline',{}).get('frac'),v.get('l2'),v.get('accuracy')) for k,v in d['configs'].items()})"
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:"hermite" -s 1 -c 1 -o gpurun_out/prof_hermite python -c "
+timeout 600 ncu -f --set full --clock-control none --import-source on -k regex:"hermite" -s 1 -c 1 -o gpurun_out/prof_hermite python -c "
 import torch
 from paper_2504_07637_b200 import hermite_coulomb, workloads as W
 b=W.shell_pairs(4096, seed=21, device='cuda'); k=W.shell_pairs(4096, seed=22, device='cuda')
