@@ -199,6 +199,17 @@ ragged_kernel(const T* __restrict__ X, const uint8_t* __restrict__ NM,
       if (kTwoSets) load(px, pn, poff, plast_off);
       else load(x, n, goff, last_off);
     }
+    // fp32: L2 prefetch of the chunk after that one (one 32-byte sector per lane
+    // and array where the chunk has that many): the mid-iteration reload then
+    // hits L2 (0.751 -> 0.742 ms; fp64: with either prefetch form 1.44-1.47 vs
+    // 1.42 ms)
+    if (!kTwoSets && c + wstride < nfull) {
+      constexpr int XS = CH * (int)sizeof(T) / 32, OS = CH * 8 / 32, NS = (CH + 31) / 32;
+      const int64_t j1 = (c + wstride) * CH;
+      if (lane < OS) prefetch_l2(OFF + j1 + lane * 4);
+      if (lane < XS) prefetch_l2(X + j1 + lane * (32 / (int)sizeof(T)));
+      if (lane < NS) prefetch_l2(NM + j1 + lane * 32);
+    }
   };
   // hot-path bound on x: below every staged order's x_up (fp64: the upward
   // ladder then never runs in the chunk path; such x take the general path)
