@@ -512,8 +512,8 @@ static boys_status launch_soa_quad(const T* x, int64_t N, T* out, T* expx, int64
                                    int64_t base, cudaStream_t s) {
   const int64_t ntiles = (N + 4 * kThreads - 1) / (4 * kThreads);
   // n = 0, up to 2^22 points: the speculative kernel (a stream of 2^20-point
-  // launches: 7.16 vs 7.68 us per launch; three resident blocks, no spills:
-  // four measured 7.29 us).  Larger launches gain nothing at their boundaries
+  // launches: 6.9 vs 7.7 us per launch; three resident blocks, no spills: four
+  // measured 1.8% slower).  Larger launches gain nothing at their boundaries
   // and pay the re-read (2^26 points: +1.2-2.5%), so they keep the plain kernel.
   if constexpr (n == 0) {
     if (N <= (int64_t(1) << 22)) {
