@@ -63,6 +63,8 @@ struct RaggedSmem {
 // measured 1.8% faster than queueing.
 template <typename T> constexpr bool kDeferUp = sizeof(T) == 4;
 
+// (Two queued elements per lane, 64 per call, so that a lane's two chains
+// interleave: 1.54 vs 1.42 ms f64, 0.79 vs 0.75 ms f32.)
 // Evaluate up to 32 queued elements (one per lane), writing straight to
 // global memory; returns the new queue length.  Out of line: it runs once per
 // ~7 chunks of an ERI-like batch, and inlined into the chunk loop its
